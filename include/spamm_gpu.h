@@ -1,0 +1,153 @@
+/*
+ * spamm_gpu.h -- C ABI of the B200-native SpAMM hot path.
+ *
+ * This is the drop-in boundary under the reference's C++ API
+ * (/root/reference/proj/core/include/spamm/{quadtree,multiply,error_control}.hpp).
+ * Plain pointers, sizes and status codes only: no C++ types, no torch types,
+ * no exception crosses it.  The C++ drop-in (include/spamm/*.hpp, namespace
+ * spamm) and the Python bindings (paper_2005_10680_b200/_native.py) both sit
+ * on top of exactly these entry points.
+ *
+ * Each entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj/core).
+ *
+ * Ownership: the caller owns every host buffer; the library owns every
+ * device buffer behind the opaque handles.  Matrices are immutable once built
+ * (quadtree.hpp:30-33).  Calls on one context are serialised by the library.
+ *
+ * Errors: every function returns SPG_OK or a negative-free status code;
+ * spg_last_error() gives the thread-local message of the last failure.  The
+ * codes map onto the reference's exception types:
+ *   SPG_EINVAL  std::invalid_argument  (dimension/leaf mismatch multiply.cpp:94-98,
+ *               error_control.cpp:161-163; tau < 0 multiply.cpp:112;
+ *               delta <= 0 error_control.cpp:205; grid error_control.cpp:139-150;
+ *               duplicate coordinates quadtree.cpp:213-216)
+ *   SPG_ERANGE  std::out_of_range      (coordinates quadtree.cpp:202-208)
+ */
+#ifndef SPAMM_GPU_H
+#define SPAMM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPG_OK 0
+#define SPG_EINVAL 1
+#define SPG_ERANGE 2
+#define SPG_ENOMEM 3
+#define SPG_ECUDA 4
+#define SPG_ENCCL 5
+#define SPG_EINTERNAL 6
+
+typedef struct spg_context spg_context; /* one device + one stream + workspace */
+typedef struct spg_matrix spg_matrix;   /* device-resident quadtree matrix     */
+
+typedef struct {
+  int32_t dimension;        /* QuadTreeMatrix::dimension()         quadtree.hpp:65 */
+  int32_t padded_dimension; /* QuadTreeMatrix::padded_dimension()  quadtree.hpp:66 */
+  int32_t leaf_size;        /* QuadTreeMatrix::leaf_size()         quadtree.hpp:67 */
+  int32_t depth;            /* log2(padded / leaf)                               */
+  int64_t nnz_blocks;       /* QuadTreeMatrix::nnz_blocks()        quadtree.hpp:79 */
+  double frobenius_norm;    /* QuadTreeMatrix::frobenius_norm()    quadtree.hpp:72 */
+} spg_matrix_info;
+
+typedef struct {
+  int64_t candidates;    /* non-null leaf pairs (A(i,k), B(k,j))                 */
+  int64_t survivors;     /* leaf products performed, |S(tau)|                    */
+  int64_t output_blocks; /* C blocks with at least one surviving product        */
+  double flops;          /* 2 * L^3 * survivors                                  */
+  float ms_tasklist;     /* device time: skip test + compaction + grouping       */
+  float ms_gemm;         /* device time: leaf GEMM kernel                         */
+  float ms_finalize;     /* device time: C norms, zero-collapse, norm pyramid    */
+} spg_spamm_stats;
+
+typedef struct {
+  double tau;            /* ControlledProduct::chosen_tau   error_control.hpp:66 */
+  int32_t tau_index;     /* grid index, -1 = exact fallback (tau = 0)           */
+  double bound;          /* ControlledProduct::bound        error_control.hpp:68 */
+  double cse_seconds;    /* ControlledProduct::cse_seconds  error_control.hpp:69 */
+  double spamm_seconds;  /* ControlledProduct::spamm_seconds error_control.hpp:70 */
+  float ms_cse;          /* device time of the tau-sweep kernels                 */
+  spg_spamm_stats spamm;
+} spg_controlled_stats;
+
+/* ---- library / context -------------------------------------------------- */
+const char* spg_last_error(void);
+int spg_version(void);
+int spg_device_count(int* count);
+int spg_context_create(int device, spg_context** out);
+int spg_context_destroy(spg_context* ctx);
+/* cudaStream_t of the context, for callers that time kernels with events. */
+int spg_context_stream(spg_context* ctx, void** stream);
+int spg_context_synchronize(spg_context* ctx);
+/* Kernel launches issued by this context so far (evidence counter). */
+int spg_context_launch_count(spg_context* ctx, int64_t* launches);
+
+/* ---- matrices (quadtree.hpp / quadtree.cpp) ------------------------------ */
+/* Replaces QuadTreeMatrix::from_coordinates at leaf granularity
+ * (quadtree.cpp:198-222): `n_leaves` dense L*L column-major blocks at block
+ * coordinates (block_rows[t], block_cols[t]).  All-zero blocks collapse
+ * (node_ops.hpp:40-53); norms are cached bottom-up (node_ops.hpp:24-36).
+ * Host buffers. */
+int spg_matrix_upload(spg_context* ctx, int32_t dimension, int32_t leaf_size, int64_t n_leaves,
+                      const int32_t* block_rows, const int32_t* block_cols, const double* payload,
+                      spg_matrix** out);
+/* Same with device-resident inputs (the matrix takes a private copy). */
+int spg_matrix_upload_device(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                             int64_t n_leaves, const int32_t* d_block_rows,
+                             const int32_t* d_block_cols, const double* d_payload,
+                             spg_matrix** out);
+/* QuadTreeMatrix::from_dense (quadtree.cpp:224-229); host row-major n x n. */
+int spg_matrix_from_dense(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                          const double* dense_rowmajor, spg_matrix** out);
+/* QuadTreeMatrix::zero (quadtree.cpp:237-240). */
+int spg_matrix_zero(spg_context* ctx, int32_t dimension, int32_t leaf_size, spg_matrix** out);
+int spg_matrix_get_info(const spg_matrix* m, spg_matrix_info* out);
+/* Non-null leaves in Morton order (child index 2*row+col, quadtree.cpp:103-106):
+ * block coordinates, L*L column-major payload and cached norms.  Any output
+ * may be NULL.  Host buffers of nnz_blocks entries. */
+int spg_matrix_download(const spg_matrix* m, int32_t* block_rows, int32_t* block_cols,
+                        double* payload, double* norms);
+/* QuadTreeMatrix::to_dense (quadtree.cpp:243-247); host row-major n x n. */
+int spg_matrix_to_dense(const spg_matrix* m, double* dense_rowmajor);
+/* Cached node norms of one tree level as a dense Morton grid of 4^level
+ * doubles; -1.0 marks an identically-zero (null) quadrant. */
+int spg_matrix_level_norms(const spg_matrix* m, int32_t level, double* out);
+int spg_matrix_free(spg_matrix* m);
+
+/* ---- hot path (error_control.hpp / multiply.hpp) ------------------------- */
+/* Validation of ToleranceGrid(std::vector<double>) (error_control.cpp:139-150). */
+int spg_tolerance_grid_check(const double* taus, int32_t n_taus);
+/* spamm::cse (error_control.hpp:44, error_control.cpp:160-166).  Bit-identical
+ * bounds.  `bounds` is a host buffer of n_taus doubles. */
+int spg_cse(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, const double* taus,
+            int32_t n_taus, double* bounds);
+/* spamm::select_tolerance (error_control.hpp:48-49, error_control.cpp:168-172).
+ * Host-only; *tau = 0 and *index = -1 when no candidate qualifies. */
+int spg_select_tolerance(const double* bounds, const double* taus, int32_t n_taus, double delta,
+                         double* tau, int32_t* index);
+/* spamm::spamm_multiply (multiply.hpp:28-29, multiply.cpp:109-116). */
+int spg_spamm(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+              spg_matrix** c, spg_spamm_stats* stats);
+/* spamm::multiply_exact (multiply.hpp:22, multiply.cpp:102-107). */
+int spg_multiply_exact(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                       spg_matrix** c, spg_spamm_stats* stats);
+/* spamm::spamm_with_error_control (error_control.hpp:76-77,
+ * error_control.cpp:203-220).  `bounds` (optional, n_taus doubles) receives
+ * the sweep. */
+int spg_spamm_with_error_control(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                                 double delta, const double* taus, int32_t n_taus,
+                                 spg_matrix** c, double* bounds, spg_controlled_stats* stats);
+/* The surviving leaf-product set of spamm_multiply(a, b, tau) (the leaves the
+ * recursion of multiply.cpp:70-92 reaches) as (i, k, j) block triples sorted
+ * by (Morton(i, j), k).  Writes min(count, capacity) triples. */
+int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                  int64_t* count, int32_t* triples, int64_t capacity);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPAMM_GPU_H */

@@ -1,0 +1,194 @@
+"""CPU checkers for the SpAMM hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs may import this package, and only as the checker (never as the thing
+measured for the GPU arm, never as a fallback).
+
+Two interchangeable back ends with the same methods:
+  * ``Oracle("port")`` -- oracle/liboracle.so, the plain-C restatement
+    (spamm_oracle.c), built from this repo; travels to the GPU box.
+  * ``Oracle("ref")``  -- oracle/_ref/libspamm_ref.so, the UNMODIFIED reference
+    core sources compiled in place by oracle/Makefile (only where
+    /root/reference exists; the built .so travels, the sources do not).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+PORT_LIB = HERE / "liboracle.so"
+REF_LIB = HERE / "_ref" / "libspamm_ref.so"
+REFERENCE_ROOT = Path("/root/reference")
+
+_i32p = C.POINTER(C.c_int32)
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+def build(ref: bool | None = None) -> None:
+    """make -C oracle (and the reference build when its sources are present)."""
+    targets = ["all"]
+    if ref or (ref is None and REFERENCE_ROOT.exists()):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", str(HERE)] + targets, check=True)
+
+
+def available(kind: str) -> bool:
+    return (PORT_LIB if kind == "port" else REF_LIB).exists()
+
+
+def _p(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class Tree:
+    def __init__(self, owner: "Oracle", handle: int, leaf: int):
+        self.owner = owner
+        self.h = handle
+        self.leaf = leaf
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.owner._free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def nnz_blocks(self) -> int:
+        return self.owner._nnz(self.h)
+
+    def frobenius(self) -> float:
+        return self.owner._frob(self.h)
+
+    def depth(self) -> int:
+        return self.owner._depth(self.h)
+
+    def leaves(self, payload: bool = True):
+        n = self.nnz_blocks()
+        rows = np.empty(n, np.int32)
+        cols = np.empty(n, np.int32)
+        norms = np.empty(n, np.float64)
+        pay = np.empty((n, self.leaf * self.leaf)) if payload else None
+        self.owner._leaves(self.h, _p(rows, C.c_int32), _p(cols, C.c_int32),
+                           _p(pay, C.c_double) if payload else None, _p(norms, C.c_double))
+        return rows, cols, pay, norms
+
+    def level_norms(self, level: int) -> np.ndarray:
+        out = np.empty(4 ** level)
+        self.owner._level(self.h, level, _p(out, C.c_double))
+        return out
+
+
+class Oracle:
+    def __init__(self, kind: str = "port"):
+        self.kind = kind
+        path = PORT_LIB if kind == "port" else REF_LIB
+        if not path.exists():
+            raise FileNotFoundError(f"{path} not built (oracle.build())")
+        L = C.CDLL(str(path))
+        pre = "ora_" if kind == "port" else "ref_"
+        self.L = L
+        self.pre = pre
+
+        def fn(name, res, args):
+            f = getattr(L, pre + name)
+            f.restype = res
+            f.argtypes = args
+            return f
+
+        self._build = fn("build", _vp, [C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _dp])
+        self._build_norm_only = fn("build_norm_only", _vp,
+                                   [C.c_int, C.c_int, C.c_int64, _i32p, _i32p, _dp])
+        self._free = fn("free", None, [_vp])
+        self._nnz = fn("nnz_blocks", C.c_int64, [_vp])
+        self._frob = fn("frobenius", C.c_double, [_vp])
+        self._depth = fn("depth", C.c_int, [_vp])
+        self._leaves = fn("leaves", None, [_vp, _i32p, _i32p, _dp, _dp])
+        self._level = fn("level_norms", None, [_vp, C.c_int, _dp])
+        self._cse = fn("cse", C.c_int, [_vp, _vp, _dp, C.c_int, _dp])
+        self._spamm = fn("spamm", _vp, [_vp, _vp, C.c_double, C.POINTER(C.c_int)])
+        self._exact = fn("multiply_exact", _vp, [_vp, _vp, C.POINTER(C.c_int)])
+        self._surv = fn("survivors", C.c_int64, [_vp, _vp, C.c_double, _i32p, C.c_int64])
+        if kind == "port":
+            self._select = fn("select_index", C.c_int, [_dp, C.c_int, C.c_double])
+            self._cand = fn("candidates", C.c_int64, [_vp, _vp])
+        else:
+            self._from_dense = fn("from_dense", _vp, [C.c_int, C.c_int, _dp])
+            self._threads = fn("set_max_threads", None, [C.c_int])
+            self._swec = fn("spamm_with_error_control", _vp,
+                            [_vp, _vp, C.c_double, _dp, C.c_int, _dp, _dp, _dp, _dp,
+                             C.POINTER(C.c_int)])
+
+    # -- construction ---------------------------------------------------------
+    def build(self, dimension: int, leaf: int, rows, cols, payload) -> Tree:
+        rows = np.ascontiguousarray(rows, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        payload = np.ascontiguousarray(payload, np.float64)
+        h = self._build(dimension, leaf, rows.size, _p(rows, C.c_int32), _p(cols, C.c_int32),
+                        _p(payload, C.c_double))
+        if not h:
+            raise ValueError("oracle build rejected the leaf list")
+        return Tree(self, h, leaf)
+
+    def build_norm_only(self, dimension: int, leaf: int, rows, cols, norms) -> Tree:
+        rows = np.ascontiguousarray(rows, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        norms = np.ascontiguousarray(norms, np.float64)
+        h = self._build_norm_only(dimension, leaf, rows.size, _p(rows, C.c_int32),
+                                  _p(cols, C.c_int32), _p(norms, C.c_double))
+        if not h:
+            raise ValueError("oracle build rejected the leaf list")
+        return Tree(self, h, leaf)
+
+    def set_threads(self, n: int):
+        if self.kind == "ref":
+            self._threads(n)
+
+    # -- hot path ---------------------------------------------------------------
+    def cse(self, a: Tree, b: Tree, taus) -> np.ndarray:
+        taus = np.ascontiguousarray(taus, np.float64)
+        out = np.empty(taus.size)
+        if self._cse(a.h, b.h, _p(taus, C.c_double), taus.size, _p(out, C.c_double)) != 0:
+            raise ValueError("cse: dimension or leaf size mismatch")
+        return out
+
+    @staticmethod
+    def select_index(bounds, delta: float) -> int:
+        for k, v in enumerate(bounds):
+            if v < delta:
+                return k
+        return -1
+
+    def spamm(self, a: Tree, b: Tree, tau: float) -> Tree:
+        st = C.c_int(0)
+        h = self._spamm(a.h, b.h, tau, C.byref(st))
+        if st.value != 0 or not h:
+            raise ValueError("spamm: invalid arguments")
+        return Tree(self, h, a.leaf)
+
+    def multiply_exact(self, a: Tree, b: Tree) -> Tree:
+        st = C.c_int(0)
+        h = self._exact(a.h, b.h, C.byref(st))
+        if st.value != 0 or not h:
+            raise ValueError("multiply: invalid arguments")
+        return Tree(self, h, a.leaf)
+
+    def survivors(self, a: Tree, b: Tree, tau: float) -> np.ndarray:
+        n = self._surv(a.h, b.h, tau, None, 0)
+        out = np.empty((n, 3), np.int32)
+        if n:
+            self._surv(a.h, b.h, tau, _p(out, C.c_int32), n)
+        return out
+
+
+def leaves_to_dense(n: int, leaf: int, rows, cols, payload) -> np.ndarray:
+    nb = (n + leaf - 1) // leaf
+    pad = np.zeros((nb * leaf, nb * leaf))
+    for r, c, p in zip(rows, cols, payload):
+        pad[r * leaf:(r + 1) * leaf, c * leaf:(c + 1) * leaf] = np.asarray(p).reshape(leaf, leaf).T
+    return pad[:n, :n]

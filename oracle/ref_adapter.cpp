@@ -1,0 +1,309 @@
+// ref_adapter.cpp -- C entry points over the UNMODIFIED reference sources.
+//
+// TEST INFRASTRUCTURE ONLY.  Compiled by oracle/Makefile together with the
+// reference's own core sources (/root/reference/proj/core/src/*.cpp, built in
+// place, never copied) into oracle/_ref/libspamm_ref.so with
+// -Dspamm=spamm_ref.  It exposes the same C signatures as oracle/spamm_oracle.h
+// with a `ref_` prefix so tests can pin the C restatement, and the GPU path,
+// against the reference itself.  Trees are assembled with the reference's
+// own node helpers (node_ops.hpp:40-63) and QuadTreeMatrix::wrap
+// (quadtree.hpp:87-89), so norms follow the reference rule by construction.
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <vector>
+
+#include "node_ops.hpp"
+#include "spamm/error_control.hpp"
+#include "spamm/execution.hpp"
+#include "spamm/multiply.hpp"
+#include "spamm/quadtree.hpp"
+
+namespace {
+
+using spamm::QuadTreeMatrix;
+using NodePtr = QuadTreeMatrix::NodePtr;
+using Node = QuadTreeMatrix::Node;
+
+struct RefTree {
+  QuadTreeMatrix m;
+  int depth = 0;
+};
+
+std::uint64_t morton2(std::uint32_t r, std::uint32_t c, int depth) {
+  std::uint64_t key = 0;
+  for (int b = depth - 1; b >= 0; --b) key = (key << 2) | (((r >> b) & 1u) << 1) | ((c >> b) & 1u);
+  return key;
+}
+
+int depth_of(int padded, int leaf) {
+  int d = 0;
+  while ((leaf << d) < padded) ++d;
+  return d;
+}
+
+struct Builder {
+  const std::vector<std::pair<std::uint64_t, std::int64_t>>* order;
+  const double* data;
+  std::int64_t block;
+  int depth;
+  bool norm_only;
+
+  NodePtr build(std::int64_t lo, std::int64_t hi, int level) const {
+    if (lo >= hi) return nullptr;
+    if (level == depth) {
+      const std::int64_t src = (*order)[lo].second;
+      if (norm_only) {
+        const double nrm = data[src];
+        if (nrm < 0.0) return nullptr;
+        auto n = std::make_shared<Node>();
+        n->norm = nrm;
+        n->block = {nrm};  // size-1 payload marks a leaf; cse_node never reads it
+        return n;
+      }
+      std::vector<double> blk(data + src * block, data + (src + 1) * block);
+      return spamm::detail::make_leaf(std::move(blk));
+    }
+    const int shift = 2 * (depth - level - 1);
+    std::array<NodePtr, 4> child;
+    std::int64_t start = lo;
+    for (int c = 0; c < 4; ++c) {
+      std::int64_t end = start;
+      while (end < hi && static_cast<int>(((*order)[end].first >> shift) & 3u) == c) ++end;
+      child[c] = build(start, end, level + 1);
+      start = end;
+    }
+    return spamm::detail::make_inner(std::move(child));
+  }
+};
+
+RefTree* build_common(int dimension, int leaf, std::int64_t n, const std::int32_t* rows,
+                      const std::int32_t* cols, const double* data, bool norm_only) {
+  try {
+    const QuadTreeMatrix zero = QuadTreeMatrix::zero(dimension, leaf);
+    const int depth = depth_of(zero.padded_dimension(), leaf);
+    const std::int64_t limit = (dimension + leaf - 1) / leaf;
+    std::vector<std::pair<std::uint64_t, std::int64_t>> order(static_cast<std::size_t>(n));
+    for (std::int64_t t = 0; t < n; ++t) {
+      if (rows[t] < 0 || cols[t] < 0 || rows[t] >= limit || cols[t] >= limit) return nullptr;
+      order[t] = {morton2(rows[t], cols[t], depth), t};
+    }
+    std::sort(order.begin(), order.end());
+    for (std::size_t t = 1; t < order.size(); ++t)
+      if (order[t].first == order[t - 1].first) return nullptr;
+    Builder b{&order, data, static_cast<std::int64_t>(leaf) * leaf, depth, norm_only};
+    auto* out = new RefTree;
+    out->m = QuadTreeMatrix::wrap(b.build(0, n, 0), dimension, leaf);
+    out->depth = depth;
+    return out;
+  } catch (const std::exception&) {
+    return nullptr;
+  }
+}
+
+void walk_leaves(const NodePtr& n, int level, int depth, std::int32_t r, std::int32_t c,
+                 std::int64_t block, std::int64_t& next, std::int32_t* rows, std::int32_t* cols,
+                 double* payload, double* norms) {
+  if (!n) return;
+  if (level == depth) {
+    const std::int64_t at = next++;
+    if (rows) rows[at] = r;
+    if (cols) cols[at] = c;
+    if (norms) norms[at] = n->norm;
+    if (payload) {
+      if (static_cast<std::int64_t>(n->block.size()) == block)
+        std::memcpy(payload + at * block, n->block.data(), sizeof(double) * block);
+      else
+        std::memset(payload + at * block, 0, sizeof(double) * block);
+    }
+    return;
+  }
+  for (int q = 0; q < 4; ++q)
+    walk_leaves(n->child[q], level + 1, depth, 2 * r + (q >> 1), 2 * c + (q & 1), block, next,
+                rows, cols, payload, norms);
+}
+
+void walk_level(const NodePtr& n, int level, int target, std::uint64_t key, double* out) {
+  if (!n) return;
+  if (level == target) {
+    out[key] = n->norm;
+    return;
+  }
+  for (int q = 0; q < 4; ++q) walk_level(n->child[q], level + 1, target, key * 4 + q, out);
+}
+
+std::int64_t count_leaves(const NodePtr& n, int level, int depth) {
+  if (!n) return 0;
+  if (level == depth) return 1;
+  std::int64_t s = 0;
+  for (const auto& c : n->child) s += count_leaves(c, level + 1, depth);
+  return s;
+}
+
+// The decisions of spamm_node (multiply.cpp:70-92) replayed on reference trees.
+void surv_walk(const NodePtr& a, const NodePtr& b, int level, int depth, double tau, bool skip,
+               std::int32_t I, std::int32_t K, std::int32_t J,
+               std::vector<std::array<std::int32_t, 3>>* out, std::int64_t& count) {
+  if (!a || !b) return;
+  if (skip && a->norm * b->norm < tau) return;
+  if (level == depth) {
+    ++count;
+    if (out) out->push_back({I, K, J});
+    return;
+  }
+  for (int row = 0; row < 2; ++row)
+    for (int col = 0; col < 2; ++col)
+      for (int h = 0; h < 2; ++h)
+        surv_walk(a->child[2 * row + h], b->child[2 * h + col], level + 1, depth, tau, skip,
+                  2 * I + row, 2 * K + h, 2 * J + col, out, count);
+}
+
+}  // namespace
+
+extern "C" {
+
+void* ref_build(int dimension, int leaf, std::int64_t n, const std::int32_t* rows,
+                const std::int32_t* cols, const double* payload) {
+  return build_common(dimension, leaf, n, rows, cols, payload, false);
+}
+
+void* ref_build_norm_only(int dimension, int leaf, std::int64_t n, const std::int32_t* rows,
+                          const std::int32_t* cols, const double* norms) {
+  return build_common(dimension, leaf, n, rows, cols, norms, true);
+}
+
+// QuadTreeMatrix::from_dense (quadtree.cpp:224-229) on a row-major host array.
+void* ref_from_dense(int dimension, int leaf, const double* rowmajor) {
+  try {
+    spamm::DenseMatrix d(dimension);
+    std::memcpy(d.data(), rowmajor, sizeof(double) * d.size());
+    auto* out = new RefTree;
+    out->m = QuadTreeMatrix::from_dense(d, leaf);
+    out->depth = depth_of(out->m.padded_dimension(), leaf);
+    return out;
+  } catch (const std::exception&) {
+    return nullptr;
+  }
+}
+
+void ref_free(void* t) { delete static_cast<RefTree*>(t); }
+
+void ref_set_max_threads(int threads) { spamm::exec::set_max_threads(threads); }
+
+int ref_depth(const void* t) { return static_cast<const RefTree*>(t)->depth; }
+std::int64_t ref_nnz_blocks(const void* t) {
+  const auto* r = static_cast<const RefTree*>(t);
+  return count_leaves(r->m.root(), 0, r->depth);
+}
+double ref_frobenius(const void* t) { return static_cast<const RefTree*>(t)->m.frobenius_norm(); }
+
+void ref_leaves(const void* t, std::int32_t* rows, std::int32_t* cols, double* payload,
+                double* norms) {
+  const auto* r = static_cast<const RefTree*>(t);
+  std::int64_t next = 0;
+  walk_leaves(r->m.root(), 0, r->depth, 0, 0,
+              static_cast<std::int64_t>(r->m.leaf_size()) * r->m.leaf_size(), next, rows, cols,
+              payload, norms);
+}
+
+void ref_level_norms(const void* t, int level, double* out) {
+  const auto* r = static_cast<const RefTree*>(t);
+  const std::uint64_t count = 1ull << (2 * level);
+  for (std::uint64_t i = 0; i < count; ++i) out[i] = -1.0;
+  walk_level(r->m.root(), 0, level, 0, out);
+}
+
+// spamm::cse (error_control.cpp:160-166)
+int ref_cse(const void* a, const void* b, const double* taus, int n, double* bounds) {
+  try {
+    const spamm::ToleranceGrid grid(std::vector<double>(taus, taus + n));
+    const auto e = spamm::cse(static_cast<const RefTree*>(a)->m, static_cast<const RefTree*>(b)->m,
+                              grid);
+    std::memcpy(bounds, e.bounds.data(), sizeof(double) * n);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// spamm::select_tolerance (error_control.cpp:168-172); returns tau (0 = exact).
+double ref_select_tolerance(const double* bounds, const double* taus, int n, double delta) {
+  const spamm::ToleranceGrid grid(std::vector<double>(taus, taus + n));
+  return spamm::select_tolerance(spamm::ErrorBoundVector{std::vector<double>(bounds, bounds + n)},
+                                 grid, delta)
+      .tau;
+}
+
+void* ref_spamm(const void* a, const void* b, double tau, int* status) {
+  try {
+    auto* out = new RefTree;
+    out->m = spamm::spamm_multiply(static_cast<const RefTree*>(a)->m,
+                                   static_cast<const RefTree*>(b)->m, spamm::SpammTolerance{tau});
+    out->depth = static_cast<const RefTree*>(a)->depth;
+    if (status) *status = 0;
+    return out;
+  } catch (const std::exception&) {
+    if (status) *status = -1;
+    return nullptr;
+  }
+}
+
+void* ref_multiply_exact(const void* a, const void* b, int* status) {
+  try {
+    auto* out = new RefTree;
+    out->m = spamm::multiply_exact(static_cast<const RefTree*>(a)->m,
+                                   static_cast<const RefTree*>(b)->m);
+    out->depth = static_cast<const RefTree*>(a)->depth;
+    if (status) *status = 0;
+    return out;
+  } catch (const std::exception&) {
+    if (status) *status = -1;
+    return nullptr;
+  }
+}
+
+// spamm::spamm_with_error_control (error_control.cpp:203-220).
+void* ref_spamm_with_error_control(const void* a, const void* b, double delta, const double* taus,
+                                   int n, double* tau_out, double* bound_out, double* cse_seconds,
+                                   double* spamm_seconds, int* status) {
+  try {
+    const spamm::ToleranceGrid grid(std::vector<double>(taus, taus + n));
+    auto res = spamm::spamm_with_error_control(static_cast<const RefTree*>(a)->m,
+                                               static_cast<const RefTree*>(b)->m, delta, grid);
+    auto* out = new RefTree;
+    out->m = std::move(res.matrix);
+    out->depth = static_cast<const RefTree*>(a)->depth;
+    if (tau_out) *tau_out = res.chosen_tau.tau;
+    if (bound_out) *bound_out = res.bound;
+    if (cse_seconds) *cse_seconds = res.cse_seconds;
+    if (spamm_seconds) *spamm_seconds = res.spamm_seconds;
+    if (status) *status = 0;
+    return out;
+  } catch (const std::exception&) {
+    if (status) *status = -1;
+    return nullptr;
+  }
+}
+
+std::int64_t ref_survivors(const void* a, const void* b, double tau, std::int32_t* triples,
+                           std::int64_t capacity) {
+  const auto* ra = static_cast<const RefTree*>(a);
+  const auto* rb = static_cast<const RefTree*>(b);
+  std::vector<std::array<std::int32_t, 3>> out;
+  std::int64_t count = 0;
+  surv_walk(ra->m.root(), rb->m.root(), 0, ra->depth, tau, true, 0, 0, 0,
+            triples ? &out : nullptr, count);
+  if (!triples) return count;
+  std::sort(out.begin(), out.end(), [&](const auto& x, const auto& y) {
+    const auto kx = morton2(x[0], x[2], ra->depth), ky = morton2(y[0], y[2], ra->depth);
+    return kx != ky ? kx < ky : x[1] < y[1];
+  });
+  const std::int64_t n = std::min<std::int64_t>(count, capacity);
+  for (std::int64_t i = 0; i < n; ++i)
+    for (int c = 0; c < 3; ++c) triples[3 * i + c] = out[i][c];
+  return count;
+}
+
+}  // extern "C"

@@ -1,0 +1,421 @@
+"""ctypes binding of the C ABI in include/spamm_gpu.h and include/spamm_synth.h.
+
+Python is plumbing here (tests, bench, smoke); the product boundary is the C
+ABI and the C++ drop-in above it.  The in-tree library must exist: a missing
+or unloadable ``lib/libspamm_gpu.so`` raises immediately -- there is no CPU
+fallback anywhere in the product path.
+
+Status codes map onto the reference's exception types (include/spamm_gpu.h):
+SPG_EINVAL -> ValueError (std::invalid_argument), SPG_ERANGE -> IndexError
+(std::out_of_range).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import sys
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+LIB_DIR = Path(__file__).resolve().parent / "lib"
+LIB_PATH = LIB_DIR / "libspamm_gpu.so"
+
+SPG_OK, SPG_EINVAL, SPG_ERANGE, SPG_ENOMEM, SPG_ECUDA, SPG_ENCCL, SPG_EINTERNAL = range(7)
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class SpgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[spg {code}] {msg}")
+        self.code = code
+
+
+class SpgCudaError(SpgError):
+    pass
+
+
+class MatrixInfo(C.Structure):
+    _fields_ = [("dimension", C.c_int32), ("padded_dimension", C.c_int32),
+                ("leaf_size", C.c_int32), ("depth", C.c_int32),
+                ("nnz_blocks", C.c_int64), ("frobenius_norm", C.c_double)]
+
+
+class SpammStats(C.Structure):
+    _fields_ = [("candidates", C.c_int64), ("survivors", C.c_int64),
+                ("output_blocks", C.c_int64), ("flops", C.c_double),
+                ("ms_tasklist", C.c_float), ("ms_gemm", C.c_float), ("ms_finalize", C.c_float)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class ControlledStats(C.Structure):
+    _fields_ = [("tau", C.c_double), ("tau_index", C.c_int32), ("bound", C.c_double),
+                ("cse_seconds", C.c_double), ("spamm_seconds", C.c_double),
+                ("ms_cse", C.c_float), ("spamm", SpammStats)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "spamm"}
+        d["spamm"] = self.spamm.as_dict()
+        return d
+
+
+_SIGNATURES = {
+    "spg_last_error": (C.c_char_p, []),
+    "spg_version": (C.c_int, []),
+    "spg_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "spg_context_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "spg_context_destroy": (C.c_int, [_vp]),
+    "spg_context_stream": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "spg_context_synchronize": (C.c_int, [_vp]),
+    "spg_context_launch_count": (C.c_int, [_vp, _i64p]),
+    "spg_matrix_upload": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p, _dp,
+                                    C.POINTER(_vp)]),
+    "spg_matrix_upload_device": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _vp, _vp, _vp,
+                                           C.POINTER(_vp)]),
+    "spg_matrix_from_dense": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.POINTER(_vp)]),
+    "spg_matrix_zero": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "spg_matrix_get_info": (C.c_int, [_vp, C.POINTER(MatrixInfo)]),
+    "spg_matrix_download": (C.c_int, [_vp, _i32p, _i32p, _dp, _dp]),
+    "spg_matrix_to_dense": (C.c_int, [_vp, _dp]),
+    "spg_matrix_level_norms": (C.c_int, [_vp, C.c_int32, _dp]),
+    "spg_matrix_free": (C.c_int, [_vp]),
+    "spg_tolerance_grid_check": (C.c_int, [_dp, C.c_int32]),
+    "spg_cse": (C.c_int, [_vp, _vp, _vp, _dp, C.c_int32, _dp]),
+    "spg_select_tolerance": (C.c_int, [_dp, _dp, C.c_int32, C.c_double, _dp, _i32p]),
+    "spg_spamm": (C.c_int, [_vp, _vp, _vp, C.c_double, C.POINTER(_vp), C.POINTER(SpammStats)]),
+    "spg_multiply_exact": (C.c_int, [_vp, _vp, _vp, C.POINTER(_vp), C.POINTER(SpammStats)]),
+    "spg_spamm_with_error_control": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
+                                               C.POINTER(_vp), _dp, C.POINTER(ControlledStats)]),
+    "spg_survivors": (C.c_int, [_vp, _vp, _vp, C.c_double, _i64p, _i32p, C.c_int64]),
+    "spg_synth_chain_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double,
+                                       C.c_int64, _i32p, _i32p, _dp, _i64p]),
+    "spg_synth_cluster_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                         C.c_uint64, C.c_uint64, C.c_double, C.c_int64, _i32p,
+                                         _i32p, _dp, _i64p]),
+    "spg_synth_chain_device": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double, C.c_uint64,
+                                         C.c_double, C.POINTER(_vp)]),
+    "spg_synth_cluster_device": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                           C.c_uint64, C.c_uint64, C.c_double, C.POINTER(_vp)]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree library (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(the CUDA path has no fallback)")
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def _check(rc: int):
+    if rc == SPG_OK:
+        return
+    msg = lib().spg_last_error().decode(errors="replace")
+    if rc == SPG_EINVAL:
+        raise ValueError(msg)
+    if rc == SPG_ERANGE:
+        raise IndexError(msg)
+    if rc == SPG_ENOMEM:
+        raise MemoryError(msg)
+    if rc == SPG_ECUDA:
+        raise SpgCudaError(rc, msg)
+    raise SpgError(rc, msg)
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    try:
+        _check(lib().spg_device_count(C.byref(n)))
+    except SpgCudaError:
+        return 0
+    return n.value
+
+
+class Context:
+    """One device, one stream (the library serialises calls per context)."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        _check(lib().spg_context_create(device, C.byref(h)))
+        self._h = h
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self) -> int:
+        s = _vp()
+        _check(lib().spg_context_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        _check(lib().spg_context_synchronize(self._h))
+
+    def launch_count(self) -> int:
+        n = C.c_int64(0)
+        _check(lib().spg_context_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().spg_context_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        # At interpreter exit the CUDA runtime may already be torn down;
+        # leaking device memory then is harmless, calling into it is not.
+        if sys.is_finalizing():
+            return
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Matrix:
+    """Device-resident quadtree matrix handle (immutable)."""
+
+    def __init__(self, ctx: Context, handle):
+        self.ctx = ctx
+        self._h = handle
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> MatrixInfo:
+        out = MatrixInfo()
+        _check(lib().spg_matrix_get_info(self._h, C.byref(out)))
+        return out
+
+    @property
+    def dimension(self):
+        return self.info().dimension
+
+    @property
+    def leaf_size(self):
+        return self.info().leaf_size
+
+    @property
+    def nnz_blocks(self):
+        return self.info().nnz_blocks
+
+    @property
+    def frobenius_norm(self):
+        return self.info().frobenius_norm
+
+    def download(self, payload: bool = True):
+        """(rows, cols, payload[n, L*L] column-major, norms) in Morton order."""
+        inf = self.info()
+        n, LL = inf.nnz_blocks, inf.leaf_size * inf.leaf_size
+        rows = np.empty(n, np.int32)
+        cols = np.empty(n, np.int32)
+        norms = np.empty(n, np.float64)
+        pay = np.empty((n, LL), np.float64) if payload else None
+        _check(lib().spg_matrix_download(self._h, _ptr(rows, C.c_int32), _ptr(cols, C.c_int32),
+                                         _ptr(pay, C.c_double) if payload else None,
+                                         _ptr(norms, C.c_double)))
+        return rows, cols, pay, norms
+
+    def to_dense(self) -> np.ndarray:
+        n = self.info().dimension
+        out = np.empty((n, n), np.float64)
+        _check(lib().spg_matrix_to_dense(self._h, _ptr(out, C.c_double)))
+        return out
+
+    def level_norms(self, level: int) -> np.ndarray:
+        out = np.empty(4 ** level, np.float64)
+        _check(lib().spg_matrix_level_norms(self._h, level, _ptr(out, C.c_double)))
+        return out
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().spg_matrix_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        if sys.is_finalizing():
+            return
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def upload(ctx: Context, dimension: int, leaf_size: int, rows, cols, payload) -> Matrix:
+    rows = np.ascontiguousarray(rows, np.int32)
+    cols = np.ascontiguousarray(cols, np.int32)
+    payload = np.ascontiguousarray(payload, np.float64)
+    n = rows.shape[0]
+    if cols.shape[0] != n or payload.size != n * leaf_size * leaf_size:
+        raise ValueError("leaf arrays disagree in length")
+    h = _vp()
+    _check(lib().spg_matrix_upload(ctx.handle, dimension, leaf_size, n, _ptr(rows, C.c_int32),
+                                   _ptr(cols, C.c_int32), _ptr(payload, C.c_double), C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def upload_device(ctx: Context, dimension: int, leaf_size: int, n_leaves: int, d_rows: int,
+                  d_cols: int, d_payload: int) -> Matrix:
+    h = _vp()
+    _check(lib().spg_matrix_upload_device(ctx.handle, dimension, leaf_size, n_leaves, d_rows,
+                                          d_cols, d_payload, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def from_dense(ctx: Context, dense: np.ndarray, leaf_size: int) -> Matrix:
+    dense = np.ascontiguousarray(dense, np.float64)
+    h = _vp()
+    _check(lib().spg_matrix_from_dense(ctx.handle, dense.shape[0], leaf_size,
+                                       _ptr(dense, C.c_double), C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def zero(ctx: Context, dimension: int, leaf_size: int) -> Matrix:
+    h = _vp()
+    _check(lib().spg_matrix_zero(ctx.handle, dimension, leaf_size, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def tolerance_grid_check(taus):
+    taus = np.ascontiguousarray(taus, np.float64)
+    _check(lib().spg_tolerance_grid_check(_ptr(taus, C.c_double), taus.size))
+
+
+def cse(ctx: Context, a: Matrix, b: Matrix, taus) -> np.ndarray:
+    taus = np.ascontiguousarray(taus, np.float64)
+    out = np.empty(taus.size, np.float64)
+    _check(lib().spg_cse(ctx.handle, a.handle, b.handle, _ptr(taus, C.c_double), taus.size,
+                         _ptr(out, C.c_double)))
+    return out
+
+
+def select_tolerance(bounds, taus, delta: float):
+    bounds = np.ascontiguousarray(bounds, np.float64)
+    taus = np.ascontiguousarray(taus, np.float64)
+    tau = C.c_double(0)
+    idx = C.c_int32(-1)
+    _check(lib().spg_select_tolerance(_ptr(bounds, C.c_double), _ptr(taus, C.c_double),
+                                      taus.size, delta, C.byref(tau), C.byref(idx)))
+    return tau.value, idx.value
+
+
+def spamm(ctx: Context, a: Matrix, b: Matrix, tau: float):
+    h = _vp()
+    st = SpammStats()
+    _check(lib().spg_spamm(ctx.handle, a.handle, b.handle, tau, C.byref(h), C.byref(st)))
+    return Matrix(ctx, h), st.as_dict()
+
+
+def multiply_exact(ctx: Context, a: Matrix, b: Matrix):
+    h = _vp()
+    st = SpammStats()
+    _check(lib().spg_multiply_exact(ctx.handle, a.handle, b.handle, C.byref(h), C.byref(st)))
+    return Matrix(ctx, h), st.as_dict()
+
+
+def spamm_with_error_control(ctx: Context, a: Matrix, b: Matrix, delta: float, taus):
+    taus = np.ascontiguousarray(taus, np.float64)
+    bounds = np.empty(taus.size, np.float64)
+    h = _vp()
+    st = ControlledStats()
+    _check(lib().spg_spamm_with_error_control(ctx.handle, a.handle, b.handle, delta,
+                                              _ptr(taus, C.c_double), taus.size, C.byref(h),
+                                              _ptr(bounds, C.c_double), C.byref(st)))
+    return Matrix(ctx, h), st.as_dict(), bounds
+
+
+def survivors(ctx: Context, a: Matrix, b: Matrix, tau: float) -> np.ndarray:
+    count = C.c_int64(0)
+    _check(lib().spg_survivors(ctx.handle, a.handle, b.handle, tau, C.byref(count), None, 0))
+    out = np.empty((count.value, 3), np.int32)
+    if count.value:
+        _check(lib().spg_survivors(ctx.handle, a.handle, b.handle, tau, C.byref(count),
+                                   _ptr(out, C.c_int32), count.value))
+    return out
+
+
+# ---------------------------------------------------------------- synthetic inputs
+def _host_synth(fn, *args):
+    n = C.c_int64(0)
+    _check(fn(*args, 0, None, None, None, C.byref(n)))
+    total = n.value
+    leaf = args[1]
+    rows = np.empty(total, np.int32)
+    cols = np.empty(total, np.int32)
+    pay = np.empty((total, leaf * leaf), np.float64)
+    _check(fn(*args, total, _ptr(rows, C.c_int32), _ptr(cols, C.c_int32),
+              _ptr(pay, C.c_double), C.byref(n)))
+    return rows, cols, pay
+
+
+def synth_chain_host(n: int, leaf: int, ell: float, seed: int, drop: float):
+    return _host_synth(lib().spg_synth_chain_host, n, leaf, ell, seed, drop)
+
+
+def synth_cluster_host(n: int, leaf: int, ell: float, density: float, site_seed: int,
+                       value_seed: int, drop: float):
+    return _host_synth(lib().spg_synth_cluster_host, n, leaf, ell, density, site_seed,
+                       value_seed, drop)
+
+
+def synth_chain_device(ctx: Context, n: int, leaf: int, ell: float, seed: int,
+                       drop: float) -> Matrix:
+    h = _vp()
+    _check(lib().spg_synth_chain_device(ctx.handle, n, leaf, ell, seed, drop, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def synth_cluster_device(ctx: Context, n: int, leaf: int, ell: float, density: float,
+                         site_seed: int, value_seed: int, drop: float) -> Matrix:
+    h = _vp()
+    _check(lib().spg_synth_cluster_device(ctx.handle, n, leaf, ell, density, site_seed,
+                                          value_seed, drop, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def dense_to_leaves(dense: np.ndarray, leaf: int):
+    """Host-side build_from_dense (quadtree.cpp:89-108) as a leaf list:
+    column-major blocks inside the logical dimension, all-zero blocks dropped."""
+    n = dense.shape[0]
+    nb = (n + leaf - 1) // leaf
+    pad = np.zeros((nb * leaf, nb * leaf))
+    pad[:n, :n] = dense
+    blocks = pad.reshape(nb, leaf, nb, leaf).transpose(0, 2, 3, 1)  # [br, bc, col, row]
+    flat = blocks.reshape(nb, nb, leaf * leaf)
+    nz = np.any(flat != 0.0, axis=2)
+    br, bc = np.nonzero(nz)
+    return br.astype(np.int32), bc.astype(np.int32), np.ascontiguousarray(flat[br, bc])
+
+
+def leaves_to_dense(n: int, leaf: int, rows, cols, payload) -> np.ndarray:
+    nb = (n + leaf - 1) // leaf
+    pad = np.zeros((nb * leaf, nb * leaf))
+    for r, c, p in zip(rows, cols, payload):
+        pad[r * leaf:(r + 1) * leaf, c * leaf:(c + 1) * leaf] = p.reshape(leaf, leaf).T
+    return pad[:n, :n]

@@ -1,0 +1,203 @@
+// common.cuh -- shared state, error plumbing and index helpers for the
+// B200-native SpAMM library (libspamm_gpu.so).
+//
+// GPU quadtree layout:
+//   * leaf payload: n_slots dense L x L FP64 blocks, column-major
+//     (quadtree.cpp:93-99), in upload order; `slots` maps the Morton-sorted
+//     non-null leaves to payload slots.
+//   * grid_slot: dense Morton grid (4^depth int32) of the leaf level, payload
+//     slot or -1 for an identically-zero (null) quadrant.
+//   * pyramid: dense Morton grids of node norms for every level 0..depth,
+//     concatenated (level l has 4^l doubles at offset (4^l - 1) / 3); -1.0
+//     marks null.  Children of Morton node m at level l are 4m..4m+3 at level
+//     l+1 in child-index order 2*row+col (node_ops.hpp:20), so every subtree
+//     is a contiguous range at every level.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spamm_gpu.h"
+
+namespace spg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg);
+void set_last_error(const std::string& msg);
+
+#define SPG_CUDA(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      ::spg::fail(SPG_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" +  \
+                                 __FILE__ + ":" + std::to_string(__LINE__) + ")");         \
+  } while (0)
+
+#define SPG_CHECK_LAUNCH(ctx)                \
+  do {                                       \
+    SPG_CUDA(cudaGetLastError());            \
+    (ctx)->launches++;                       \
+  } while (0)
+
+constexpr int kMaxDepth = 14;  // 4^14 Morton grid entries = 268M (2.1 GB norms) at most
+
+}  // namespace spg
+
+struct spg_context {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[8] = {};
+  std::mutex mu;
+  int64_t launches = 0;
+  // persistent scratch (grown on demand, stream-ordered)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+};
+
+struct spg_matrix {
+  spg_context* ctx = nullptr;
+  int32_t dimension = 0, padded = 0, leaf = 0, depth = 0;
+  int64_t nnzb = 0;     // non-null leaves
+  int64_t n_slots = 0;  // payload slots (>= nnzb)
+  double* payload = nullptr;    // n_slots * L * L
+  uint64_t* keys = nullptr;     // nnzb Morton keys, ascending
+  int32_t* slots = nullptr;     // nnzb payload slots, aligned with keys
+  int32_t* grid_slot = nullptr; // 4^depth
+  double* pyramid = nullptr;    // sum_l 4^l
+  double frob = 0.0;
+};
+
+namespace spg {
+
+__host__ __device__ inline int64_t level_offset(int level) { return ((int64_t(1) << (2 * level)) - 1) / 3; }
+__host__ __device__ inline int64_t pyramid_size(int depth) { return level_offset(depth + 1); }
+
+__host__ __device__ inline uint64_t spread2(uint32_t x) {
+  uint64_t v = x;
+  v = (v | (v << 16)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v << 8)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v << 4)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+__host__ __device__ inline uint32_t compact2(uint64_t v) {
+  v &= 0x5555555555555555ull;
+  v = (v | (v >> 1)) & 0x3333333333333333ull;
+  v = (v | (v >> 2)) & 0x0F0F0F0F0F0F0F0Full;
+  v = (v | (v >> 4)) & 0x00FF00FF00FF00FFull;
+  v = (v | (v >> 8)) & 0x0000FFFF0000FFFFull;
+  v = (v | (v >> 16)) & 0x00000000FFFFFFFFull;
+  return static_cast<uint32_t>(v);
+}
+// Morton key with the row bit above the column bit at every level, so the
+// two key bits of a level are the child index 2*row+col (node_ops.hpp:20).
+__host__ __device__ inline uint64_t morton2(uint32_t row, uint32_t col) {
+  return (spread2(row) << 1) | spread2(col);
+}
+__host__ __device__ inline uint32_t morton_row(uint64_t key) { return compact2(key >> 1); }
+__host__ __device__ inline uint32_t morton_col(uint64_t key) { return compact2(key); }
+
+// Stream-ordered device buffer.
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t count, cudaStream_t stream) : n(count), s(stream) {
+    if (count) SPG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    reset();
+    p = o.p; n = o.n; s = o.s;
+    o.p = nullptr; o.n = 0;
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* release() { T* r = p; p = nullptr; n = 0; return r; }
+  T* get() const { return p; }
+};
+
+template <typename T>
+T* dev_alloc(size_t count, cudaStream_t s) {
+  T* p = nullptr;
+  if (count) SPG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
+  return p;
+}
+
+inline unsigned grid_for(int64_t work, int threads, int64_t cap = (int64_t(1) << 30)) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return static_cast<unsigned>(g);
+}
+
+// Scoped context lock + device guard.
+struct CtxGuard {
+  std::lock_guard<std::mutex> lock;
+  explicit CtxGuard(spg_context* c) : lock(c->mu) { SPG_CUDA(cudaSetDevice(c->device)); }
+};
+
+// --- internal entry points shared between translation units -------------
+// norms.cu
+void leaf_norms(spg_context* ctx, const double* payload, int64_t n_slots, int leaf,
+                int32_t dimension, int32_t nb_logical, const int32_t* slot_rows,
+                const int32_t* slot_cols, double* norms, uint8_t* nonzero, int* bad_padding);
+void build_pyramid(spg_context* ctx, spg_matrix* m, const double* slot_norms,
+                   const uint8_t* slot_nonzero);
+// matrix.cu
+spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32_t leaf,
+                                      int64_t n_leaves, const int32_t* d_rows,
+                                      const int32_t* d_cols, double* d_payload_owned);
+spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32_t leaf,
+                                      int64_t n_blocks, uint64_t* d_keys_owned,
+                                      double* d_payload_owned);
+void matrix_destroy(spg_matrix* m);
+void check_shape(int32_t dimension, int32_t leaf, int32_t* padded, int32_t* depth);
+// cse.cu
+void cse_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, const double* taus,
+                int n_taus, double* bounds_host, float* ms);
+// spamm.cu
+spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                         bool skip_test, spg_spamm_stats* stats);
+
+int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
+
+}  // namespace spg
+
+// Wrap an API body: translate exceptions to status codes + last error.
+#define SPG_API_BEGIN try {
+#define SPG_API_END                                        \
+  return SPG_OK;                                           \
+  }                                                        \
+  catch (const ::spg::Error& e) {                          \
+    ::spg::set_last_error(e.what());                       \
+    return e.code;                                         \
+  }                                                        \
+  catch (const std::bad_alloc&) {                          \
+    ::spg::set_last_error("out of host memory");           \
+    return SPG_ENOMEM;                                     \
+  }                                                        \
+  catch (const std::exception& e) {                        \
+    ::spg::set_last_error(e.what());                       \
+    return SPG_EINTERNAL;                                  \
+  }

@@ -1,0 +1,504 @@
+// matrix.cu -- device-resident quadtree matrices: build (upload), inspect,
+// download; the context and error plumbing of the C ABI.
+//
+// Reference interfaces replaced: QuadTreeMatrix::from_coordinates /
+// from_dense / zero / to_dense / nnz_blocks / frobenius_norm
+// (quadtree.hpp:52-83, quadtree.cpp:198-247).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+
+#include <thrust/iterator/counting_iterator.h>
+
+#include "common.cuh"
+
+namespace spg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d) {
+  int64_t h = 0;
+  SPG_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+// padded_dimension_for (quadtree.cpp:15-22) + validate_shape (:55-58).
+void check_shape(int32_t dimension, int32_t leaf, int32_t* padded, int32_t* depth) {
+  if (dimension <= 0) fail(SPG_EINVAL, "dimension must be positive");
+  if (leaf <= 0) fail(SPG_EINVAL, "leaf_size must be positive");
+  int64_t p = leaf;
+  int d = 0;
+  while (p < dimension) {
+    if (p > (int64_t(1) << 29)) fail(SPG_EINVAL, "dimension too large to pad");
+    p *= 2;
+    ++d;
+  }
+  if (d > kMaxDepth) fail(SPG_EINVAL, "quadtree depth exceeds the device grid limit");
+  *padded = static_cast<int32_t>(p);
+  *depth = d;
+}
+
+namespace {
+
+// Scatter uploaded leaves into the Morton grid; detects range errors
+// (std::out_of_range, quadtree.cpp:202-208) and duplicates
+// (std::invalid_argument, quadtree.cpp:213-216).
+__global__ void scatter_leaves(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                               int64_t n, int32_t nb_logical, int32_t* __restrict__ grid_slot,
+                               int* __restrict__ flags) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int32_t r = rows[t], c = cols[t];
+  if (r < 0 || c < 0 || r >= nb_logical || c >= nb_logical) {
+    atomicOr(flags, 1);
+    return;
+  }
+  const uint64_t key = morton2(static_cast<uint32_t>(r), static_cast<uint32_t>(c));
+  const int32_t prev = atomicCAS(grid_slot + key, -1, static_cast<int32_t>(t));
+  if (prev != -1) atomicOr(flags, 2);
+}
+
+__global__ void scatter_keys(const uint64_t* __restrict__ keys, int64_t n,
+                             int32_t* __restrict__ grid_slot, int32_t* __restrict__ rows,
+                             int32_t* __restrict__ cols) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint64_t key = keys[t];
+  grid_slot[key] = static_cast<int32_t>(t);
+  rows[t] = static_cast<int32_t>(morton_row(key));
+  cols[t] = static_cast<int32_t>(morton_col(key));
+}
+
+struct NonNull {
+  const int32_t* grid;
+  __host__ __device__ bool operator()(const uint64_t& p) const { return grid[p] >= 0; }
+};
+
+__global__ void gather_slots(const uint64_t* __restrict__ keys, int64_t n,
+                             const int32_t* __restrict__ grid_slot, int32_t* __restrict__ slots) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  slots[t] = grid_slot[keys[t]];
+}
+
+// Compact the non-null grid positions into (keys, slots), ascending Morton.
+void compact_leaves(spg_context* ctx, spg_matrix* m) {
+  const int64_t count = int64_t(1) << (2 * m->depth);
+  DevBuf<uint64_t> keys(std::max<int64_t>(count, 1), ctx->stream);
+  DevBuf<int64_t> n_sel(1, ctx->stream);
+  thrust::counting_iterator<uint64_t> it(0);
+  size_t tmp_bytes = 0;
+  SPG_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, it, keys.get(), n_sel.get(), count,
+                                 NonNull{m->grid_slot}, ctx->stream));
+  DevBuf<uint8_t> tmp(tmp_bytes, ctx->stream);
+  SPG_CUDA(cub::DeviceSelect::If(tmp.get(), tmp_bytes, it, keys.get(), n_sel.get(), count,
+                                 NonNull{m->grid_slot}, ctx->stream));
+  ctx->launches++;
+  m->nnzb = copy_scalar_to_host_i64(ctx, n_sel.get());
+  m->keys = dev_alloc<uint64_t>(std::max<int64_t>(m->nnzb, 1), ctx->stream);
+  m->slots = dev_alloc<int32_t>(std::max<int64_t>(m->nnzb, 1), ctx->stream);
+  if (m->nnzb) {
+    SPG_CUDA(cudaMemcpyAsync(m->keys, keys.get(), m->nnzb * sizeof(uint64_t),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+    gather_slots<<<grid_for(m->nnzb, 256), 256, 0, ctx->stream>>>(m->keys, m->nnzb, m->grid_slot,
+                                                                  m->slots);
+    SPG_CHECK_LAUNCH(ctx);
+  }
+}
+
+spg_matrix* new_matrix(spg_context* ctx, int32_t dimension, int32_t leaf) {
+  auto m = std::make_unique<spg_matrix>();
+  m->ctx = ctx;
+  m->dimension = dimension;
+  m->leaf = leaf;
+  check_shape(dimension, leaf, &m->padded, &m->depth);
+  const int64_t cells = int64_t(1) << (2 * m->depth);
+  m->grid_slot = dev_alloc<int32_t>(cells, ctx->stream);
+  SPG_CUDA(cudaMemsetAsync(m->grid_slot, 0xff, cells * sizeof(int32_t), ctx->stream));
+  m->pyramid = dev_alloc<double>(pyramid_size(m->depth), ctx->stream);
+  return m.release();
+}
+
+void finish_matrix(spg_context* ctx, spg_matrix* m, const int32_t* slot_rows,
+                   const int32_t* slot_cols, bool check_padding) {
+  const int32_t nb_logical = (m->dimension + m->leaf - 1) / m->leaf;
+  DevBuf<double> norms(std::max<int64_t>(m->n_slots, 1), ctx->stream);
+  DevBuf<uint8_t> nonzero(std::max<int64_t>(m->n_slots, 1), ctx->stream);
+  DevBuf<int> bad(1, ctx->stream);
+  SPG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx->stream));
+  leaf_norms(ctx, m->payload, m->n_slots, m->leaf, m->dimension, nb_logical,
+             check_padding ? slot_rows : nullptr, slot_cols, norms.get(), nonzero.get(),
+             bad.get());
+  int h_bad = 0;
+  SPG_CUDA(cudaMemcpyAsync(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  build_pyramid(ctx, m, norms.get(), nonzero.get());
+  compact_leaves(ctx, m);  // synchronises
+  if (h_bad) fail(SPG_EINVAL, "nonzero entry in the padding region of a boundary leaf");
+  double root = -1.0;
+  SPG_CUDA(cudaMemcpyAsync(&root, m->pyramid, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  m->frob = root < 0.0 ? 0.0 : root;
+}
+
+__global__ void gather_payload(const double* __restrict__ payload,
+                               const int32_t* __restrict__ slots, int64_t n, int64_t elems,
+                               double* __restrict__ out) {
+  const int64_t leaf = blockIdx.y + static_cast<int64_t>(gridDim.y) * blockIdx.z;
+  if (leaf >= n) return;
+  const double* src = payload + static_cast<int64_t>(slots[leaf]) * elems;
+  double* dst = out + leaf * elems;
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < elems;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[e] = src[e];
+}
+
+__global__ void gather_norms(const uint64_t* __restrict__ keys, int64_t n,
+                             const double* __restrict__ level, double* __restrict__ out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  out[t] = level[keys[t]];
+}
+
+}  // namespace
+
+void matrix_destroy(spg_matrix* m) {
+  if (!m) return;
+  cudaStream_t s = m->ctx->stream;
+  cudaSetDevice(m->ctx->device);
+  if (m->payload) cudaFreeAsync(m->payload, s);
+  if (m->keys) cudaFreeAsync(m->keys, s);
+  if (m->slots) cudaFreeAsync(m->slots, s);
+  if (m->grid_slot) cudaFreeAsync(m->grid_slot, s);
+  if (m->pyramid) cudaFreeAsync(m->pyramid, s);
+  delete m;
+}
+
+spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32_t leaf,
+                                      int64_t n_leaves, const int32_t* d_rows,
+                                      const int32_t* d_cols, double* d_payload_owned) {
+  std::unique_ptr<spg_matrix, void (*)(spg_matrix*)> m(nullptr, matrix_destroy);
+  try {
+    m.reset(new_matrix(ctx, dimension, leaf));
+  } catch (...) {
+    if (d_payload_owned) cudaFreeAsync(d_payload_owned, ctx->stream);
+    throw;
+  }
+  m->payload = d_payload_owned;
+  m->n_slots = n_leaves;
+  if (n_leaves > (int64_t(1) << 31) - 1) fail(SPG_EINVAL, "too many leaves");
+  const int32_t nb_logical = (dimension + leaf - 1) / leaf;
+  DevBuf<int> flags(1, ctx->stream);
+  SPG_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int), ctx->stream));
+  if (n_leaves) {
+    scatter_leaves<<<grid_for(n_leaves, 256), 256, 0, ctx->stream>>>(
+        d_rows, d_cols, n_leaves, nb_logical, m->grid_slot, flags.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  int h_flags = 0;
+  SPG_CUDA(cudaMemcpyAsync(&h_flags, flags.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h_flags & 1) fail(SPG_ERANGE, "block coordinate outside the matrix dimension");
+  if (h_flags & 2) fail(SPG_EINVAL, "duplicate block coordinate");
+  finish_matrix(ctx, m.get(), d_rows, d_cols, true);
+  return m.release();
+}
+
+spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32_t leaf,
+                                      int64_t n_blocks, uint64_t* d_keys_owned,
+                                      double* d_payload_owned) {
+  std::unique_ptr<spg_matrix, void (*)(spg_matrix*)> m(nullptr, matrix_destroy);
+  try {
+    m.reset(new_matrix(ctx, dimension, leaf));
+  } catch (...) {
+    if (d_payload_owned) cudaFreeAsync(d_payload_owned, ctx->stream);
+    if (d_keys_owned) cudaFreeAsync(d_keys_owned, ctx->stream);
+    throw;
+  }
+  m->payload = d_payload_owned;
+  m->n_slots = n_blocks;
+  DevBuf<uint64_t> keys;
+  keys.p = d_keys_owned;
+  keys.n = n_blocks;
+  keys.s = ctx->stream;
+  DevBuf<int32_t> rows(std::max<int64_t>(n_blocks, 1), ctx->stream);
+  DevBuf<int32_t> cols(std::max<int64_t>(n_blocks, 1), ctx->stream);
+  if (n_blocks) {
+    scatter_keys<<<grid_for(n_blocks, 256), 256, 0, ctx->stream>>>(
+        d_keys_owned, n_blocks, m->grid_slot, rows.get(), cols.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  finish_matrix(ctx, m.get(), rows.get(), cols.get(), false);
+  return m.release();
+}
+
+}  // namespace spg
+
+using namespace spg;
+
+extern "C" {
+
+const char* spg_last_error(void) { return spg::g_last_error.c_str(); }
+
+int spg_version(void) { return 1; }
+
+int spg_device_count(int* count) {
+  SPG_API_BEGIN
+  if (!count) fail(SPG_EINVAL, "null output");
+  *count = 0;
+  SPG_CUDA(cudaGetDeviceCount(count));
+  SPG_API_END
+}
+
+int spg_context_create(int device, spg_context** out) {
+  SPG_API_BEGIN
+  if (!out) fail(SPG_EINVAL, "null output");
+  *out = nullptr;
+  auto ctx = std::make_unique<spg_context>();
+  ctx->device = device;
+  SPG_CUDA(cudaSetDevice(device));
+  SPG_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
+  SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  for (auto& e : ctx->ev) SPG_CUDA(cudaEventCreate(&e));
+  // Keep freed device memory cached in the pool (stream-ordered allocator).
+  cudaMemPool_t pool;
+  SPG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t threshold = UINT64_MAX;
+  SPG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+  *out = ctx.release();
+  SPG_API_END
+}
+
+int spg_context_destroy(spg_context* ctx) {
+  SPG_API_BEGIN
+  if (!ctx) return SPG_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  SPG_API_END
+}
+
+int spg_context_stream(spg_context* ctx, void** stream) {
+  SPG_API_BEGIN
+  if (!ctx || !stream) fail(SPG_EINVAL, "null argument");
+  *stream = ctx->stream;
+  SPG_API_END
+}
+
+int spg_context_synchronize(spg_context* ctx) {
+  SPG_API_BEGIN
+  if (!ctx) fail(SPG_EINVAL, "null context");
+  CtxGuard g(ctx);
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  SPG_API_END
+}
+
+int spg_context_launch_count(spg_context* ctx, int64_t* launches) {
+  SPG_API_BEGIN
+  if (!ctx || !launches) fail(SPG_EINVAL, "null argument");
+  *launches = ctx->launches;
+  SPG_API_END
+}
+
+int spg_matrix_upload(spg_context* ctx, int32_t dimension, int32_t leaf_size, int64_t n_leaves,
+                      const int32_t* block_rows, const int32_t* block_cols, const double* payload,
+                      spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_leaves < 0) fail(SPG_EINVAL, "negative leaf count");
+  if (n_leaves && (!block_rows || !block_cols || !payload)) fail(SPG_EINVAL, "null leaf arrays");
+  CtxGuard g(ctx);
+  int32_t padded, depth;
+  check_shape(dimension, leaf_size, &padded, &depth);
+  const int64_t elems = static_cast<int64_t>(leaf_size) * leaf_size;
+  DevBuf<int32_t> rows(std::max<int64_t>(n_leaves, 1), ctx->stream);
+  DevBuf<int32_t> cols(std::max<int64_t>(n_leaves, 1), ctx->stream);
+  double* d_payload = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx->stream);
+  DevBuf<double> payload_guard;
+  payload_guard.p = d_payload;
+  payload_guard.n = 1;
+  payload_guard.s = ctx->stream;
+  if (n_leaves) {
+    SPG_CUDA(cudaMemcpyAsync(rows.get(), block_rows, n_leaves * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(cols.get(), block_cols, n_leaves * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(d_payload, payload, n_leaves * elems * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->stream));
+  }
+  payload_guard.release();
+  *out = matrix_from_device_leaves(ctx, dimension, leaf_size, n_leaves, rows.get(), cols.get(),
+                                   d_payload);
+  SPG_API_END
+}
+
+int spg_matrix_upload_device(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                             int64_t n_leaves, const int32_t* d_block_rows,
+                             const int32_t* d_block_cols, const double* d_payload,
+                             spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_leaves < 0) fail(SPG_EINVAL, "negative leaf count");
+  CtxGuard g(ctx);
+  int32_t padded, depth;
+  check_shape(dimension, leaf_size, &padded, &depth);
+  const int64_t elems = static_cast<int64_t>(leaf_size) * leaf_size;
+  double* copy = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx->stream);
+  if (n_leaves)
+    SPG_CUDA(cudaMemcpyAsync(copy, d_payload, n_leaves * elems * sizeof(double),
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+  *out = matrix_from_device_leaves(ctx, dimension, leaf_size, n_leaves, d_block_rows,
+                                   d_block_cols, copy);
+  SPG_API_END
+}
+
+int spg_matrix_from_dense(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                          const double* dense, spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out || !dense) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  int32_t padded, depth;
+  check_shape(dimension, leaf_size, &padded, &depth);
+  // build_from_dense (quadtree.cpp:89-108): leaf blocks inside the logical
+  // dimension, column-major; padding stays zero; all-zero leaves dropped.
+  const int32_t nb = (dimension + leaf_size - 1) / leaf_size;
+  const int64_t elems = static_cast<int64_t>(leaf_size) * leaf_size;
+  std::vector<int32_t> rows, cols;
+  std::vector<double> payload;
+  std::vector<double> blk(static_cast<size_t>(elems));
+  for (int32_t br = 0; br < nb; ++br)
+    for (int32_t bc = 0; bc < nb; ++bc) {
+      std::fill(blk.begin(), blk.end(), 0.0);
+      const int r = std::min(leaf_size, dimension - br * leaf_size);
+      const int c = std::min(leaf_size, dimension - bc * leaf_size);
+      bool any = false;
+      for (int j = 0; j < c; ++j)
+        for (int i = 0; i < r; ++i) {
+          const double v =
+              dense[static_cast<int64_t>(br * leaf_size + i) * dimension + bc * leaf_size + j];
+          blk[i + static_cast<size_t>(j) * leaf_size] = v;
+          any = any || v != 0.0;
+        }
+      if (!any) continue;
+      rows.push_back(br);
+      cols.push_back(bc);
+      payload.insert(payload.end(), blk.begin(), blk.end());
+    }
+  return spg_matrix_upload(ctx, dimension, leaf_size, static_cast<int64_t>(rows.size()),
+                           rows.data(), cols.data(), payload.data(), out);
+  SPG_API_END
+}
+
+int spg_matrix_zero(spg_context* ctx, int32_t dimension, int32_t leaf_size, spg_matrix** out) {
+  return spg_matrix_upload(ctx, dimension, leaf_size, 0, nullptr, nullptr, nullptr, out);
+}
+
+int spg_matrix_get_info(const spg_matrix* m, spg_matrix_info* out) {
+  SPG_API_BEGIN
+  if (!m || !out) fail(SPG_EINVAL, "null argument");
+  out->dimension = m->dimension;
+  out->padded_dimension = m->padded;
+  out->leaf_size = m->leaf;
+  out->depth = m->depth;
+  out->nnz_blocks = m->nnzb;
+  out->frobenius_norm = m->frob;
+  SPG_API_END
+}
+
+int spg_matrix_download(const spg_matrix* m, int32_t* block_rows, int32_t* block_cols,
+                        double* payload, double* norms) {
+  SPG_API_BEGIN
+  if (!m) fail(SPG_EINVAL, "null matrix");
+  spg_context* ctx = m->ctx;
+  CtxGuard g(ctx);
+  if (m->nnzb == 0) return SPG_OK;
+  std::vector<uint64_t> keys(static_cast<size_t>(m->nnzb));
+  SPG_CUDA(cudaMemcpyAsync(keys.data(), m->keys, m->nnzb * sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  if (payload) {
+    const int64_t elems = static_cast<int64_t>(m->leaf) * m->leaf;
+    // chunked gather + copy keeps the staging buffer bounded
+    const int64_t chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (elems * 8));
+    DevBuf<double> stage(std::min(chunk, m->nnzb) * elems, ctx->stream);
+    for (int64_t lo = 0; lo < m->nnzb; lo += chunk) {
+      const int64_t n = std::min(chunk, m->nnzb - lo);
+      dim3 grid(static_cast<unsigned>(std::min<int64_t>((elems + 255) / 256, 64)),
+                static_cast<unsigned>(std::min<int64_t>(n, 65535)),
+                static_cast<unsigned>((n + 65534) / 65535));
+      gather_payload<<<grid, 256, 0, ctx->stream>>>(m->payload, m->slots + lo, n, elems,
+                                                    stage.get());
+      SPG_CHECK_LAUNCH(ctx);
+      SPG_CUDA(cudaMemcpyAsync(payload + lo * elems, stage.get(), n * elems * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    }
+  }
+  if (norms) {
+    DevBuf<double> d_norms(m->nnzb, ctx->stream);
+    gather_norms<<<grid_for(m->nnzb, 256), 256, 0, ctx->stream>>>(
+        m->keys, m->nnzb, m->pyramid + level_offset(m->depth), d_norms.get());
+    SPG_CHECK_LAUNCH(ctx);
+    SPG_CUDA(cudaMemcpyAsync(norms, d_norms.get(), m->nnzb * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int64_t t = 0; t < m->nnzb; ++t) {
+    if (block_rows) block_rows[t] = static_cast<int32_t>(morton_row(keys[t]));
+    if (block_cols) block_cols[t] = static_cast<int32_t>(morton_col(keys[t]));
+  }
+  SPG_API_END
+}
+
+int spg_matrix_to_dense(const spg_matrix* m, double* dense) {
+  SPG_API_BEGIN
+  if (!m || !dense) fail(SPG_EINVAL, "null argument");
+  const int64_t n = m->dimension, L = m->leaf, elems = L * L;
+  std::vector<int32_t> rows(static_cast<size_t>(m->nnzb)), cols(static_cast<size_t>(m->nnzb));
+  std::vector<double> payload(static_cast<size_t>(m->nnzb * elems));
+  int rc = spg_matrix_download(m, rows.data(), cols.data(), payload.data(), nullptr);
+  if (rc != SPG_OK) return rc;
+  std::memset(dense, 0, sizeof(double) * static_cast<size_t>(n * n));
+  for (int64_t t = 0; t < m->nnzb; ++t) {
+    const int64_t r0 = rows[t] * L, c0 = cols[t] * L;
+    for (int64_t j = 0; j < L && c0 + j < n; ++j)
+      for (int64_t i = 0; i < L && r0 + i < n; ++i)
+        dense[(r0 + i) * n + c0 + j] = payload[t * elems + i + j * L];
+  }
+  SPG_API_END
+}
+
+int spg_matrix_level_norms(const spg_matrix* m, int32_t level, double* out) {
+  SPG_API_BEGIN
+  if (!m || !out) fail(SPG_EINVAL, "null argument");
+  if (level < 0 || level > m->depth) fail(SPG_EINVAL, "level outside the tree");
+  spg_context* ctx = m->ctx;
+  CtxGuard g(ctx);
+  SPG_CUDA(cudaMemcpyAsync(out, m->pyramid + level_offset(level),
+                           (int64_t(1) << (2 * level)) * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  SPG_API_END
+}
+
+int spg_matrix_free(spg_matrix* m) {
+  SPG_API_BEGIN
+  if (!m) return SPG_OK;
+  std::lock_guard<std::mutex> lock(m->ctx->mu);
+  matrix_destroy(m);
+  SPG_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,365 @@
+// spamm.cu -- K4 task-list builder, K5 dispatch, C finalisation, and the
+// product entry points of the C ABI.
+//
+// K4: the surviving leaf products are exactly the leaves the
+// reference recursion spamm_node (multiply.cpp:70-92) reaches: the skip test
+// !(fl(nA*nB) < tau) is applied top-down at EVERY level (root included) on
+// the dense norm pyramids, so even the underflow corner where an inner norm is
+// below a child's (sqrt(fl(x*x)) < x for subnormal squares) skips exactly what
+// the reference skips.  The leaf level writes sort keys
+// (Morton(i,j) << depth) | k; a deterministic radix sort groups them by
+// output block in Morton order with k ascending; run heads give each output
+// block's [begin, end) range of (A slot, B slot) pairs for K5.
+//
+// C (multiply.cpp:16-20, quadtree.cpp:24-36): one leaf per output block with
+// >= 1 survivor; its norm follows block_norm (K1); all-zero sums collapse to
+// null (make_leaf); inner norms follow combine_child_norms (K2).
+#include <chrono>
+
+#include <thrust/iterator/counting_iterator.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "triples.cuh"
+
+namespace spg {
+
+namespace {
+
+__global__ void head_flags(const uint64_t* __restrict__ keys, int64_t n, int kbits,
+                           uint8_t* __restrict__ flags) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  flags[t] = (t == 0) || ((keys[t] >> kbits) != (keys[t - 1] >> kbits));
+}
+
+__global__ void run_outputs(const uint64_t* __restrict__ keys, const int64_t* __restrict__ heads,
+                            int64_t n_out, int64_t n_surv, int kbits,
+                            uint64_t* __restrict__ out_keys, int64_t* __restrict__ out_offset) {
+  const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o > n_out) return;
+  if (o == n_out) {
+    out_offset[o] = n_surv;
+    return;
+  }
+  const int64_t h = heads[o];
+  out_offset[o] = h;
+  out_keys[o] = keys[h] >> kbits;
+}
+
+__global__ void make_pairs(const uint64_t* __restrict__ keys, int64_t n, int kbits,
+                           const int32_t* __restrict__ gridA, const int32_t* __restrict__ gridB,
+                           int2* __restrict__ pairs) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint64_t key = keys[t];
+  const uint32_t k = static_cast<uint32_t>(key & ((uint64_t(1) << kbits) - 1));
+  const uint64_t ij = key >> kbits;
+  const uint32_t i = morton_row(ij), j = morton_col(ij);
+  pairs[t] = make_int2(gridA[morton2(i, k)], gridB[morton2(k, j)]);
+}
+
+__global__ void count_by_index(const uint64_t* __restrict__ keys, int64_t n, bool use_col,
+                               int32_t* __restrict__ counts) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t idx = use_col ? morton_col(keys[t]) : morton_row(keys[t]);
+  atomicAdd(counts + idx, 1);
+}
+
+__global__ void count_products(const int32_t* __restrict__ colA, const int32_t* __restrict__ rowB,
+                               int n, int64_t* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  out[k] = static_cast<int64_t>(colA[k]) * rowB[k];
+}
+
+struct TaskList {
+  DevBuf<uint64_t> keys;       // sorted survivor keys
+  int64_t n_surv = 0;
+  int kbits = 0;
+};
+
+// Surviving (i,k,j) leaf products, sorted by (Morton(i,j), k).
+template <KeepRule R>
+TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau) {
+  const int d = a->depth;
+  TaskList tl;
+  tl.kbits = d;
+  TripleList cur = root_list<R>(ctx, a, b, tau);
+  DevBuf<uint64_t> keys;
+  if (d == 0) {
+    tl.n_surv = cur.n;
+    keys = DevBuf<uint64_t>(1, ctx->stream);
+    SPG_CUDA(cudaMemsetAsync(keys.get(), 0, sizeof(uint64_t), ctx->stream));
+  } else {
+    for (int l = 0; l < d - 1 && cur.n > 0; ++l) {
+      TripleList next = expand_level<R>(ctx, cur, a->pyramid + level_offset(l + 1),
+                                        b->pyramid + level_offset(l + 1), tau);
+      cur = std::move(next);
+    }
+    // last level: write sort keys directly
+    const int64_t n = cur.n;
+    DevBuf<uint8_t> masks(std::max<int64_t>(n, 1), ctx->stream);
+    DevBuf<int64_t> counts(n + 1, ctx->stream);
+    DevBuf<int64_t> offsets(n + 1, ctx->stream);
+    SPG_CUDA(cudaMemsetAsync(counts.get() + n, 0, sizeof(int64_t), ctx->stream));
+    if (n) {
+      expand_count<R><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+          cur.I.get(), cur.K.get(), cur.J.get(), n, a->pyramid + level_offset(d),
+          b->pyramid + level_offset(d), tau, masks.get(), counts.get());
+      SPG_CHECK_LAUNCH(ctx);
+    }
+    tl.n_surv = scan_counts(ctx, counts.get(), n, offsets.get());
+    keys = DevBuf<uint64_t>(std::max<int64_t>(tl.n_surv, 1), ctx->stream);
+    if (tl.n_surv) {
+      expand_write_keys<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
+          cur.I.get(), cur.K.get(), cur.J.get(), n, masks.get(), offsets.get(), d, keys.get());
+      SPG_CHECK_LAUNCH(ctx);
+    }
+  }
+  if (tl.n_surv > 1) {
+    DevBuf<uint64_t> sorted(tl.n_surv, ctx->stream);
+    size_t bytes = 0;
+    const int end_bit = std::max(1, 3 * d);
+    SPG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys.get(), sorted.get(), tl.n_surv,
+                                            0, end_bit, ctx->stream));
+    DevBuf<uint8_t> tmp(bytes, ctx->stream);
+    SPG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, keys.get(), sorted.get(),
+                                            tl.n_surv, 0, end_bit, ctx->stream));
+    ctx->launches++;
+    keys = std::move(sorted);
+  }
+  tl.keys = std::move(keys);
+  return tl;
+}
+
+int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix* b) {
+  const int nb = 1 << a->depth;
+  DevBuf<int32_t> colA(nb, ctx->stream), rowB(nb, ctx->stream);
+  DevBuf<int64_t> prod(nb, ctx->stream), total(1, ctx->stream);
+  SPG_CUDA(cudaMemsetAsync(colA.get(), 0, nb * sizeof(int32_t), ctx->stream));
+  SPG_CUDA(cudaMemsetAsync(rowB.get(), 0, nb * sizeof(int32_t), ctx->stream));
+  if (a->nnzb) {
+    count_by_index<<<grid_for(a->nnzb, 256), 256, 0, ctx->stream>>>(a->keys, a->nnzb, true,
+                                                                    colA.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  if (b->nnzb) {
+    count_by_index<<<grid_for(b->nnzb, 256), 256, 0, ctx->stream>>>(b->keys, b->nnzb, false,
+                                                                    rowB.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  count_products<<<grid_for(nb, 256), 256, 0, ctx->stream>>>(colA.get(), rowB.get(), nb,
+                                                             prod.get());
+  SPG_CHECK_LAUNCH(ctx);
+  size_t bytes = 0;
+  SPG_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, prod.get(), total.get(), nb, ctx->stream));
+  DevBuf<uint8_t> tmp(bytes, ctx->stream);
+  SPG_CUDA(cub::DeviceReduce::Sum(tmp.get(), bytes, prod.get(), total.get(), nb, ctx->stream));
+  ctx->launches++;
+  return copy_scalar_to_host_i64(ctx, total.get());
+}
+
+template <int L, int KC, int WM, int WN, int NSTAGE>
+void launch_dmma(spg_context* ctx, const double* A, const double* B, const int2* pairs,
+                 const int64_t* out_offset, int64_t n_out, double* C) {
+  using Cfg = DmmaGemmCfg<L, KC, WM, WN, NSTAGE>;
+  auto kern = leaf_gemm_dmma<L, KC, WM, WN, NSTAGE>;
+  SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::kSmemBytes)));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, ctx->stream>>>(A, B, pairs, out_offset, n_out, C);
+  SPG_CHECK_LAUNCH(ctx);
+}
+
+void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const int2* pairs,
+              const int64_t* out_offset, int64_t n_out, double* C) {
+  if (n_out == 0) return;
+  switch (L) {
+    case 32:
+      launch_dmma<32, 32, 16, 8, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+      break;
+    case 64:
+      launch_dmma<64, 32, 32, 16, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+      break;
+    case 128:
+      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+      break;
+    default: {
+      const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
+      leaf_gemm_generic<<<grid, 256, 0, ctx->stream>>>(A, B, pairs, out_offset, n_out, L, C);
+      SPG_CHECK_LAUNCH(ctx);
+    }
+  }
+}
+
+}  // namespace
+
+spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                         bool skip_test, spg_spamm_stats* stats) {
+  if (a->dimension != b->dimension || a->leaf != b->leaf)
+    fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
+  if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
+  const int L = a->leaf;
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau)
+                          : build_tasklist<KeepRule::kExact>(ctx, a, b, tau);
+  const int64_t n_surv = tl.n_surv;
+  // group by output block
+  int64_t n_out = 0;
+  DevBuf<uint64_t> out_keys;
+  DevBuf<int64_t> out_offset;
+  DevBuf<int2> pairs;
+  if (n_surv) {
+    DevBuf<uint8_t> flags(n_surv, ctx->stream);
+    head_flags<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
+                                                              flags.get());
+    SPG_CHECK_LAUNCH(ctx);
+    DevBuf<int64_t> heads(n_surv, ctx->stream);
+    DevBuf<int64_t> n_sel(1, ctx->stream);
+    thrust::counting_iterator<int64_t> it(0);
+    size_t bytes = 0;
+    SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags.get(), heads.get(), n_sel.get(),
+                                        n_surv, ctx->stream));
+    DevBuf<uint8_t> tmp(bytes, ctx->stream);
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flags.get(), heads.get(),
+                                        n_sel.get(), n_surv, ctx->stream));
+    ctx->launches++;
+    n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
+    out_keys = DevBuf<uint64_t>(n_out, ctx->stream);
+    out_offset = DevBuf<int64_t>(n_out + 1, ctx->stream);
+    run_outputs<<<grid_for(n_out + 1, 256), 256, 0, ctx->stream>>>(
+        tl.keys.get(), heads.get(), n_out, n_surv, tl.kbits, out_keys.get(), out_offset.get());
+    SPG_CHECK_LAUNCH(ctx);
+    pairs = DevBuf<int2>(n_surv, ctx->stream);
+    make_pairs<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
+                                                              a->grid_slot, b->grid_slot,
+                                                              pairs.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  tl.keys.reset();
+  SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+  double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx->stream);
+  run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload);
+  SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+  pairs.reset();
+  out_offset.reset();
+  spg_matrix* c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, out_keys.release(),
+                                            c_payload);
+  SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+  SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
+  if (stats) {
+    stats->survivors = n_surv;
+    stats->output_blocks = n_out;
+    stats->flops = 2.0 * static_cast<double>(L) * L * L * static_cast<double>(n_surv);
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_tasklist, ctx->ev[2], ctx->ev[3]));
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_gemm, ctx->ev[3], ctx->ev[4]));
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_finalize, ctx->ev[4], ctx->ev[5]));
+    stats->candidates = count_candidates(ctx, a, b);
+  }
+  return c;
+}
+
+}  // namespace spg
+
+using namespace spg;
+
+namespace {
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+}  // namespace
+
+extern "C" {
+
+int spg_spamm(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+              spg_matrix** c, spg_spamm_stats* stats) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !c) fail(SPG_EINVAL, "null argument");
+  *c = nullptr;
+  CtxGuard g(ctx);
+  *c = spamm_device(ctx, a, b, tau, true, stats);
+  SPG_API_END
+}
+
+int spg_multiply_exact(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                       spg_matrix** c, spg_spamm_stats* stats) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !c) fail(SPG_EINVAL, "null argument");
+  *c = nullptr;
+  CtxGuard g(ctx);
+  *c = spamm_device(ctx, a, b, 0.0, false, stats);
+  SPG_API_END
+}
+
+int spg_spamm_with_error_control(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                                 double delta, const double* taus, int32_t n_taus,
+                                 spg_matrix** c, double* bounds, spg_controlled_stats* stats) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !c) fail(SPG_EINVAL, "null argument");
+  *c = nullptr;
+  // error_control.cpp:205
+  if (!(delta > 0.0)) fail(SPG_EINVAL, "spamm_with_error_control: delta must be positive");
+  int rc = spg_tolerance_grid_check(taus, n_taus);
+  if (rc != SPG_OK) return rc;
+  CtxGuard g(ctx);
+  std::vector<double> local(static_cast<size_t>(n_taus));
+  double* bv = bounds ? bounds : local.data();
+  float cse_ms = 0.0f;
+  const auto t0 = Clock::now();
+  cse_device(ctx, a, b, taus, n_taus, bv, &cse_ms);
+  const double cse_seconds = seconds_since(t0);
+  int32_t k = -1;
+  for (int32_t i = 0; i < n_taus; ++i)
+    if (bv[i] < delta) {
+      k = i;
+      break;
+    }
+  const double tau = k >= 0 ? taus[k] : 0.0;
+  spg_spamm_stats ss{};
+  const auto t1 = Clock::now();
+  *c = spamm_device(ctx, a, b, tau, true, stats ? &ss : nullptr);
+  const double spamm_seconds = seconds_since(t1);
+  if (stats) {
+    stats->tau = tau;
+    stats->tau_index = k;
+    stats->bound = k >= 0 ? bv[k] : 0.0;
+    stats->cse_seconds = cse_seconds;
+    stats->spamm_seconds = spamm_seconds;
+    stats->ms_cse = cse_ms;
+    stats->spamm = ss;
+  }
+  SPG_API_END
+}
+
+int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                  int64_t* count, int32_t* triples, int64_t capacity) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !count) fail(SPG_EINVAL, "null argument");
+  if (a->dimension != b->dimension || a->leaf != b->leaf)
+    fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
+  if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
+  CtxGuard g(ctx);
+  TaskList tl = build_tasklist<KeepRule::kSkip>(ctx, a, b, tau);
+  *count = tl.n_surv;
+  if (triples && capacity > 0 && tl.n_surv > 0) {
+    const int64_t n = std::min(capacity, tl.n_surv);
+    std::vector<uint64_t> keys(static_cast<size_t>(n));
+    SPG_CUDA(cudaMemcpyAsync(keys.data(), tl.keys.get(), n * sizeof(uint64_t),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint64_t kmask = (uint64_t(1) << tl.kbits) - 1;
+    for (int64_t t = 0; t < n; ++t) {
+      const uint64_t ij = keys[t] >> tl.kbits;
+      triples[3 * t + 0] = static_cast<int32_t>(morton_row(ij));
+      triples[3 * t + 1] = static_cast<int32_t>(keys[t] & kmask);
+      triples[3 * t + 2] = static_cast<int32_t>(morton_col(ij));
+    }
+  }
+  SPG_API_END
+}
+
+}  // extern "C"
