@@ -58,7 +58,8 @@ struct spg_context {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev[8] = {};
   std::mutex mu;
-  int64_t launches = 0;
+  int64_t launches = 0;   // own kernels launched (evidence counter)
+  int64_t lib_calls = 0;  // CUB primitives invoked
   // persistent scratch (grown on demand, stream-ordered)
   void* scratch = nullptr;
   size_t scratch_bytes = 0;

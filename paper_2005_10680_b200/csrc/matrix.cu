@@ -102,7 +102,7 @@ void compact_leaves(spg_context* ctx, spg_matrix* m) {
   DevBuf<uint8_t> tmp(tmp_bytes, ctx->stream);
   SPG_CUDA(cub::DeviceSelect::If(tmp.get(), tmp_bytes, it, keys.get(), n_sel.get(), count,
                                  NonNull{m->grid_slot}, ctx->stream));
-  ctx->launches++;
+  ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   m->nnzb = copy_scalar_to_host_i64(ctx, n_sel.get());
   m->keys = dev_alloc<uint64_t>(std::max<int64_t>(m->nnzb, 1), ctx->stream);
   m->slots = dev_alloc<int32_t>(std::max<int64_t>(m->nnzb, 1), ctx->stream);

@@ -127,7 +127,7 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
     DevBuf<uint8_t> tmp(bytes, ctx->stream);
     SPG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, keys.get(), sorted.get(),
                                             tl.n_surv, 0, end_bit, ctx->stream));
-    ctx->launches++;
+    ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
     keys = std::move(sorted);
   }
   tl.keys = std::move(keys);
@@ -157,7 +157,7 @@ int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix
   SPG_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, prod.get(), total.get(), nb, ctx->stream));
   DevBuf<uint8_t> tmp(bytes, ctx->stream);
   SPG_CUDA(cub::DeviceReduce::Sum(tmp.get(), bytes, prod.get(), total.get(), nb, ctx->stream));
-  ctx->launches++;
+  ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   return copy_scalar_to_host_i64(ctx, total.get());
 }
 
@@ -226,7 +226,7 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     DevBuf<uint8_t> tmp(bytes, ctx->stream);
     SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flags.get(), heads.get(),
                                         n_sel.get(), n_surv, ctx->stream));
-    ctx->launches++;
+    ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
     n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
     out_keys = DevBuf<uint64_t>(n_out, ctx->stream);
     out_offset = DevBuf<int64_t>(n_out + 1, ctx->stream);

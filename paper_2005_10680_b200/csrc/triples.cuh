@@ -104,7 +104,7 @@ inline int64_t scan_counts(spg_context* ctx, const int64_t* counts, int64_t n, i
   SPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, offsets, n + 1, ctx->stream));
   DevBuf<uint8_t> tmp(bytes, ctx->stream);
   SPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, counts, offsets, n + 1, ctx->stream));
-  ctx->launches++;
+  ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   int64_t total = 0;
   SPG_CUDA(cudaMemcpyAsync(&total, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
                            ctx->stream));

@@ -1,0 +1,151 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle.
+
+Bars (BASELINE.json north_star / SURVEY.md 8a P1-P5): node norms, CSE bounds,
+selected tau and surviving product set bit-exact; C~ within 1e-12 relative
+Frobenius of the reference product with the identical block structure."""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, bits_equal, golden_names, load_golden
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-12  # P5: DMMA fuses and reorders the k-sum (test_multiply.cpp:55,122)
+
+
+def rel_fro(x, y):
+    ny = np.linalg.norm(y)
+    return np.linalg.norm(x - y) / (ny if ny > 0 else 1.0)
+
+
+def upload_golden(nat, ctx, g, tag):
+    return nat.upload(ctx, int(g["n"]), int(g["L"]), g[f"{tag}_rows"], g[f"{tag}_cols"],
+                      g[f"{tag}_payload"])
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names() if n != "cfg1"])
+def test_golden_case_on_gpu(ctx, name):
+    from paper_2005_10680_b200 import _native as nat
+    g = load_golden(name)
+    n, L = int(g["n"]), int(g["L"])
+    A, B = upload_golden(nat, ctx, g, "a"), upload_golden(nat, ctx, g, "b")
+    lvl = 0
+    while f"a_level{lvl}" in g:
+        assert bits_equal(A.level_norms(lvl), g[f"a_level{lvl}"]), lvl
+        assert bits_equal(B.level_norms(lvl), g[f"b_level{lvl}"]), lvl
+        lvl += 1
+    bounds = nat.cse(ctx, A, B, g["taus"])
+    assert bits_equal(bounds, g["bounds"])
+    i = 0
+    while f"delta{i}" in g:
+        tau, k = nat.select_tolerance(bounds, g["taus"], float(g[f"delta{i}"]))
+        assert k == int(g[f"select{i}"])
+        i += 1
+    i = 0
+    while f"tau{i}" in g:
+        tau = float(g[f"tau{i}"])
+        assert np.array_equal(nat.survivors(ctx, A, B, tau), g[f"surv{i}"])
+        C, st = nat.spamm(ctx, A, B, tau)
+        r, c, p, nrm = C.download()
+        assert np.array_equal(r, g[f"c{i}_rows"]) and np.array_equal(c, g[f"c{i}_cols"])
+        assert rel_fro(p, g[f"c{i}_payload"]) < REL_TOL
+        assert st["survivors"] == len(g[f"surv{i}"])
+        i += 1
+
+
+def test_cfg1_on_gpu_matches_reference_golden(ctx):
+    """BASELINE.json config 1 (N=4096, L=64, 32 taus, delta=1e-6) end to end."""
+    import hashlib
+    from paper_2005_10680_b200 import _native as nat
+    meta = json.loads((GOLDEN / "cfg1.json").read_text())
+    g = load_golden("cfg1")
+    rows, cols, pay = nat.synth_chain_host(meta["n"], meta["leaf"], meta["ell"], meta["seed"],
+                                           meta["drop"])
+    A = nat.upload(ctx, meta["n"], meta["leaf"], rows, cols, pay)
+    for lvl in range(7):
+        assert bits_equal(A.level_norms(lvl), g[f"a_level{lvl}"])
+    C, st, bounds = nat.spamm_with_error_control(ctx, A, A, meta["delta"], g["taus"])
+    assert bits_equal(bounds, g["bounds"])
+    assert st["tau_index"] == meta["tau_index"] and st["tau"] == meta["tau"]
+    assert st["bound"] == meta["bound"]
+    surv = nat.survivors(ctx, A, A, meta["tau"])
+    assert hashlib.sha256(np.ascontiguousarray(surv).tobytes()).hexdigest() == \
+        meta["survivors_sha256"]
+    assert st["spamm"]["survivors"] == meta["survivors"]
+    r, c, p, nrm = C.download()
+    assert np.array_equal(r, g["c_rows"]) and np.array_equal(c, g["c_cols"])
+    assert abs(C.frobenius_norm - float(g["c_frob"])) <= 1e-12 * float(g["c_frob"])
+    # delta bound against an exact dense product (error_control.hpp:73-75)
+    d = nat.leaves_to_dense(meta["n"], meta["leaf"], rows, cols, pay)
+    exact = d @ d
+    approx = nat.leaves_to_dense(meta["n"], meta["leaf"], r, c, p)
+    realized = np.linalg.norm(approx - exact)
+    assert realized < meta["delta"]
+    assert realized <= st["bound"] * (1 + 1e-9) + 1e-10 * np.linalg.norm(d) ** 2 * 1e-6
+
+
+def _random_case(rng, n, L, fill, decay):
+    d = np.where(rng.uniform(size=(n, n)) < fill, rng.uniform(-1, 1, (n, n)), 0.0)
+    if decay:
+        d *= np.exp(-np.abs(np.subtract.outer(np.arange(n), np.arange(n))) / decay)
+    return d
+
+
+@pytest.mark.parametrize("L", [2, 4, 8, 16, 32, 64, 128])
+def test_random_vs_oracle_all_leaf_sizes(ctx, port, L):
+    """Every GEMM instantiation (generic, DMMA L=32/64/128) and ragged sizes."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import geometric_grid
+    rng = np.random.default_rng(1000 + L)
+    for trial in range(4):
+        nb = int(rng.integers(1, 6 if L >= 64 else 9))
+        n = max(1, nb * L - int(rng.integers(0, L)))
+        da = _random_case(rng, n, L, rng.uniform(0.05, 1.0), rng.uniform(1, 3 * L))
+        db = _random_case(rng, n, L, rng.uniform(0.05, 1.0), rng.uniform(1, 3 * L))
+        la, lb = nat.dense_to_leaves(da, L), nat.dense_to_leaves(db, L)
+        A, B = nat.upload(ctx, n, L, *la), nat.upload(ctx, n, L, *lb)
+        ta, tb = port.build(n, L, *la), port.build(n, L, *lb)
+        for lvl in range(ta.depth() + 1):
+            assert bits_equal(A.level_norms(lvl), ta.level_norms(lvl))
+        taus = geometric_grid(1.0, float(rng.uniform(0.2, 0.9)), int(rng.integers(1, 80)))
+        assert bits_equal(nat.cse(ctx, A, B, taus), port.cse(ta, tb, taus))
+        for tau in (float(taus[rng.integers(0, len(taus))]), 0.0):
+            assert np.array_equal(nat.survivors(ctx, A, B, tau), port.survivors(ta, tb, tau))
+            C, _ = nat.spamm(ctx, A, B, tau)
+            r, c, p, _ = C.download()
+            ro, co, po, _ = port.spamm(ta, tb, tau).leaves()
+            assert np.array_equal(r, ro) and np.array_equal(c, co)
+            assert rel_fro(p, po) < REL_TOL
+
+
+def test_many_taus_and_piece_batches(ctx, port):
+    """Grids far larger than the tile's piece batch (350 = geometric default,
+    error_control.hpp:21, and 4000) still give bit-identical bounds."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import geometric_grid
+    rng = np.random.default_rng(5)
+    n, L = 512, 16
+    da = _random_case(rng, n, L, 1.0, 20.0)
+    la = nat.dense_to_leaves(da, L)
+    A = nat.upload(ctx, n, L, *la)
+    t = port.build(n, L, *la)
+    for taus in (geometric_grid(), geometric_grid(1.0, 0.99, 4000)):
+        assert bits_equal(nat.cse(ctx, A, A, taus), port.cse(t, t, taus))
+
+
+def test_run_to_run_determinism(ctx):
+    """SPEC determinism (test_multiply.cpp:140-156 analogue): repeated calls are
+    bitwise identical."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    rows, cols, pay = nat.synth_chain_host(2048, 64, 40.0, 3, 1e-10)
+    A = nat.upload(ctx, 2048, 64, rows, cols, pay)
+    outs = []
+    for _ in range(3):
+        C, st, b = nat.spamm_with_error_control(ctx, A, A, 1e-6, log_grid(32))
+        outs.append((b, C.download()))
+    for b, (r, c, p, nrm) in outs[1:]:
+        assert bits_equal(b, outs[0][0])
+        assert bits_equal(p, outs[0][1][2]) and bits_equal(nrm, outs[0][1][3])
