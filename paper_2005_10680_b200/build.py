@@ -35,7 +35,7 @@ HEADERS = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
 
 CXX = os.environ.get("CXX", "g++")
 DROPIN_SOURCES = ["dropin/quadtree.cpp", "dropin/multiply.cpp", "dropin/error_control.cpp",
-                  "dropin/execution.cpp", "dropin/runtime.cpp"]
+                  "dropin/runtime.cpp"]
 
 
 def _stale(target: Path, deps) -> bool:

@@ -1,0 +1,122 @@
+// error_control.cpp -- drop-in CSE sweep, selection and controlled product
+// (error_control.hpp:18-77) on the GPU path; truncate() is a host operation
+// outside the hot path (SURVEY.md 8f "next").
+#include "spamm/error_control.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+#include <utility>
+
+#include "runtime.hpp"
+
+namespace spamm {
+
+ToleranceGrid::ToleranceGrid(std::vector<double> taus) : taus_(std::move(taus)) {
+  // error_control.cpp:139-150 (same messages, same exception type)
+  if (taus_.empty()) throw std::invalid_argument("tolerance grid must be nonempty");
+  for (size_t k = 0; k < taus_.size(); ++k) {
+    if (!(taus_[k] > 0.0)) throw std::invalid_argument("tolerance grid entries must be positive");
+    if (k > 0 && !(taus_[k] < taus_[k - 1]))
+      throw std::invalid_argument("tolerance grid must be strictly decreasing");
+  }
+}
+
+ToleranceGrid ToleranceGrid::geometric(double start, double ratio, int count) {
+  if (!(start > 0.0)) throw std::invalid_argument("grid start must be positive");
+  if (!(ratio > 0.0 && ratio < 1.0)) throw std::invalid_argument("grid ratio must be in (0, 1)");
+  if (count < 1) throw std::invalid_argument("grid count must be at least 1");
+  std::vector<double> taus(static_cast<size_t>(count));
+  double tau = start;  // repeated multiplication, not pow (error_control.cpp:152-158)
+  for (int k = 0; k < count; ++k) {
+    taus[k] = tau;
+    tau *= ratio;
+  }
+  return ToleranceGrid(std::move(taus));
+}
+
+ErrorBoundVector cse(const QuadTreeMatrix& a, const QuadTreeMatrix& b, const ToleranceGrid& grid) {
+  if (a.dimension() != b.dimension() || a.leaf_size() != b.leaf_size())
+    throw std::invalid_argument("cse: dimension or leaf size mismatch");
+  ErrorBoundVector out{std::vector<double>(grid.size())};
+  b200::check(spg_cse(b200::context(), a.device(), b.device(), grid.taus().data(),
+                      static_cast<int32_t>(grid.size()), out.bounds.data()));
+  return out;
+}
+
+SpammTolerance select_tolerance(const ErrorBoundVector& bounds, const ToleranceGrid& grid,
+                                double delta) {
+  double tau = 0.0;
+  int32_t k = -1;
+  b200::check(spg_select_tolerance(bounds.bounds.data(), grid.taus().data(),
+                                   static_cast<int32_t>(grid.size()), delta, &tau, &k));
+  return SpammTolerance{tau};
+}
+
+TruncationResult truncate(const QuadTreeMatrix& x, double delta) {
+  // Greedy removal in ascending (norm, row-major position) order while the
+  // removed norm stays strictly below delta (error_control.hpp:59-62).
+  if (delta < 0.0) throw std::invalid_argument("truncate: delta must be nonnegative");
+  spg_matrix_info info{};
+  b200::check(spg_matrix_get_info(x.device(), &info));
+  const int L = x.leaf_size();
+  const size_t n = static_cast<size_t>(info.nnz_blocks);
+  std::vector<int32_t> rows(n), cols(n);
+  std::vector<double> norms(n), payload(n * static_cast<size_t>(L) * L);
+  if (n) b200::check(spg_matrix_download(x.device(), rows.data(), cols.data(), payload.data(), norms.data()));
+  const int64_t side = x.padded_dimension() / L;
+  std::vector<size_t> order(n);
+  for (size_t i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](size_t p, size_t q) {
+    const int64_t pp = rows[p] * side + cols[p], pq = rows[q] * side + cols[q];
+    return norms[p] != norms[q] ? norms[p] < norms[q] : pp < pq;
+  });
+  std::vector<char> removed(n, 0);
+  double sumsq = 0.0;
+  int64_t count = 0;
+  for (size_t i : order) {
+    if (!(std::sqrt(sumsq + norms[i] * norms[i]) < delta)) break;
+    sumsq += norms[i] * norms[i];
+    removed[i] = 1;
+    ++count;
+  }
+  TruncationResult result{x, std::sqrt(sumsq), count};
+  if (count > 0) {
+    std::vector<int32_t> kr, kc;
+    std::vector<double> kp;
+    const size_t LL = static_cast<size_t>(L) * L;
+    for (size_t i = 0; i < n; ++i)
+      if (!removed[i]) {
+        kr.push_back(rows[i]);
+        kc.push_back(cols[i]);
+        kp.insert(kp.end(), payload.begin() + i * LL, payload.begin() + (i + 1) * LL);
+      }
+    spg_matrix* m = nullptr;
+    b200::check(spg_matrix_upload(b200::context(), x.dimension(), L, static_cast<int64_t>(kr.size()),
+                                  kr.data(), kc.data(), kp.data(), &m));
+    result.matrix = adopt_device(m);
+  }
+  return result;
+}
+
+ControlledProduct spamm_with_error_control(const QuadTreeMatrix& a, const QuadTreeMatrix& b,
+                                           double delta, const ToleranceGrid& grid) {
+  if (!(delta > 0.0))
+    throw std::invalid_argument("spamm_with_error_control: delta must be positive");
+  if (a.dimension() != b.dimension() || a.leaf_size() != b.leaf_size())
+    throw std::invalid_argument("cse: dimension or leaf size mismatch");
+  spg_matrix* c = nullptr;
+  spg_controlled_stats st{};
+  b200::check(spg_spamm_with_error_control(b200::context(), a.device(), b.device(), delta,
+                                           grid.taus().data(), static_cast<int32_t>(grid.size()),
+                                           &c, nullptr, &st));
+  ControlledProduct out;
+  out.matrix = adopt_device(c);
+  out.chosen_tau = SpammTolerance{st.tau};
+  out.bound = st.bound;
+  out.cse_seconds = st.cse_seconds;
+  out.spamm_seconds = st.spamm_seconds;
+  return out;
+}
+
+}  // namespace spamm
