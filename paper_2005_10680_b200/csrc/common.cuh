@@ -17,7 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <mutex>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -52,6 +54,23 @@ constexpr int kMaxDepth = 14;  // 4^14 Morton grid entries = 268M (2.1 GB norms)
 
 }  // namespace spg
 
+namespace spg {
+// Per-context caching allocator.  Every kernel of a context runs on its one
+// stream, so a freed block can be handed to the next request immediately
+// (stream order makes the reuse safe).  The driver is only called while the
+// working set grows (warm-up); steady-state calls never allocate, which keeps
+// step times free of driver-pool stalls (measured up to 1.3 s with the
+// stream-ordered pool).
+struct DevicePool {
+  std::multimap<size_t, void*> free_blocks;
+  std::unordered_map<void*, size_t> live;
+  size_t reserved = 0;
+  void* alloc(size_t bytes, cudaStream_t s);
+  void release(void* p);
+  void trim(cudaStream_t s);
+};
+}  // namespace spg
+
 struct spg_context {
   int device = 0;
   int sm_count = 0;
@@ -60,9 +79,7 @@ struct spg_context {
   std::mutex mu;
   int64_t launches = 0;   // own kernels launched (evidence counter)
   int64_t lib_calls = 0;  // CUB primitives invoked
-  // persistent scratch (grown on demand, stream-ordered)
-  void* scratch = nullptr;
-  size_t scratch_bytes = 0;
+  spg::DevicePool pool;
 };
 
 struct spg_matrix {
@@ -109,40 +126,47 @@ __host__ __device__ inline uint64_t morton2(uint32_t row, uint32_t col) {
 __host__ __device__ inline uint32_t morton_row(uint64_t key) { return compact2(key >> 1); }
 __host__ __device__ inline uint32_t morton_col(uint64_t key) { return compact2(key); }
 
-// Stream-ordered device buffer.
+// Device buffer owned by a context's pool.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t n = 0;
-  cudaStream_t s = nullptr;
+  spg_context* c = nullptr;
   DevBuf() = default;
-  DevBuf(size_t count, cudaStream_t stream) : n(count), s(stream) {
-    if (count) SPG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), stream));
+  DevBuf(size_t count, spg_context* ctx) : n(count), c(ctx) {
+    if (count) p = static_cast<T*>(ctx->pool.alloc(count * sizeof(T), ctx->stream));
   }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), c(o.c) { o.p = nullptr; o.n = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
     reset();
-    p = o.p; n = o.n; s = o.s;
+    p = o.p; n = o.n; c = o.c;
     o.p = nullptr; o.n = 0;
     return *this;
   }
   ~DevBuf() { reset(); }
   void reset() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) c->pool.release(p);
     p = nullptr;
     n = 0;
+  }
+  // adopt a pool block allocated elsewhere
+  static DevBuf adopt(T* ptr, size_t count, spg_context* ctx) {
+    DevBuf b;
+    b.p = ptr; b.n = count; b.c = ctx;
+    return b;
   }
   T* release() { T* r = p; p = nullptr; n = 0; return r; }
   T* get() const { return p; }
 };
 
 template <typename T>
-T* dev_alloc(size_t count, cudaStream_t s) {
-  T* p = nullptr;
-  if (count) SPG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), count * sizeof(T), s));
-  return p;
+T* dev_alloc(size_t count, spg_context* ctx) {
+  return count ? static_cast<T*>(ctx->pool.alloc(count * sizeof(T), ctx->stream)) : nullptr;
+}
+inline void dev_free(void* p, spg_context* ctx) {
+  if (p) ctx->pool.release(p);
 }
 
 inline unsigned grid_for(int64_t work, int threads, int64_t cap = (int64_t(1) << 30)) {
@@ -182,6 +206,17 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
                          bool skip_test, spg_spamm_stats* stats);
 
 int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
+
+// SPG_TRACE=1: synchronising host-side phase timer printed to stderr
+// (diagnostics only; off by default, never used for reported numbers).
+struct PhaseTrace {
+  spg_context* ctx;
+  const char* what;
+  double t0;
+  bool on;
+  PhaseTrace(spg_context* c, const char* w);
+  ~PhaseTrace();
+};
 
 }  // namespace spg
 

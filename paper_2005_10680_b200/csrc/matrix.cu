@@ -7,6 +7,9 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -23,6 +26,75 @@ thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+static bool trace_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPG_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+PhaseTrace::PhaseTrace(spg_context* c, const char* w) : ctx(c), what(w), t0(0), on(trace_enabled()) {
+  if (on) {
+    cudaStreamSynchronize(ctx->stream);
+    t0 = now_ms();
+  }
+}
+PhaseTrace::~PhaseTrace() {
+  if (on) {
+    cudaStreamSynchronize(ctx->stream);
+    std::fprintf(stderr, "[spg] %-28s %9.3f ms\n", what, now_ms() - t0);
+  }
+}
+
+void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
+  bytes = (bytes + 511) & ~size_t(511);
+  // best fit among cached blocks, wasting at most half of the block
+  auto it = free_blocks.lower_bound(bytes);
+  if (it != free_blocks.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+    void* p = it->second;
+    live[p] = it->first;
+    free_blocks.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    trim(s);
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? SPG_ENOMEM : SPG_ECUDA,
+         std::string("device allocation of ") + std::to_string(bytes) +
+             " bytes failed: " + cudaGetErrorString(e));
+  }
+  reserved += bytes;
+  live[p] = bytes;
+  return p;
+}
+
+void DevicePool::release(void* p) {
+  auto it = live.find(p);
+  if (it == live.end()) return;
+  free_blocks.emplace(it->second, p);
+  live.erase(it);
+}
+
+void DevicePool::trim(cudaStream_t s) {
+  cudaStreamSynchronize(s);
+  for (auto& kv : free_blocks) {
+    cudaFree(kv.second);
+    reserved -= kv.first;
+  }
+  free_blocks.clear();
+}
 
 int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d) {
   int64_t h = 0;
@@ -93,19 +165,19 @@ __global__ void gather_slots(const uint64_t* __restrict__ keys, int64_t n,
 // Compact the non-null grid positions into (keys, slots), ascending Morton.
 void compact_leaves(spg_context* ctx, spg_matrix* m) {
   const int64_t count = int64_t(1) << (2 * m->depth);
-  DevBuf<uint64_t> keys(std::max<int64_t>(count, 1), ctx->stream);
-  DevBuf<int64_t> n_sel(1, ctx->stream);
+  DevBuf<uint64_t> keys(std::max<int64_t>(count, 1), ctx);
+  DevBuf<int64_t> n_sel(1, ctx);
   thrust::counting_iterator<uint64_t> it(0);
   size_t tmp_bytes = 0;
   SPG_CUDA(cub::DeviceSelect::If(nullptr, tmp_bytes, it, keys.get(), n_sel.get(), count,
                                  NonNull{m->grid_slot}, ctx->stream));
-  DevBuf<uint8_t> tmp(tmp_bytes, ctx->stream);
+  DevBuf<uint8_t> tmp(tmp_bytes, ctx);
   SPG_CUDA(cub::DeviceSelect::If(tmp.get(), tmp_bytes, it, keys.get(), n_sel.get(), count,
                                  NonNull{m->grid_slot}, ctx->stream));
   ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   m->nnzb = copy_scalar_to_host_i64(ctx, n_sel.get());
-  m->keys = dev_alloc<uint64_t>(std::max<int64_t>(m->nnzb, 1), ctx->stream);
-  m->slots = dev_alloc<int32_t>(std::max<int64_t>(m->nnzb, 1), ctx->stream);
+  m->keys = dev_alloc<uint64_t>(std::max<int64_t>(m->nnzb, 1), ctx);
+  m->slots = dev_alloc<int32_t>(std::max<int64_t>(m->nnzb, 1), ctx);
   if (m->nnzb) {
     SPG_CUDA(cudaMemcpyAsync(m->keys, keys.get(), m->nnzb * sizeof(uint64_t),
                              cudaMemcpyDeviceToDevice, ctx->stream));
@@ -122,18 +194,18 @@ spg_matrix* new_matrix(spg_context* ctx, int32_t dimension, int32_t leaf) {
   m->leaf = leaf;
   check_shape(dimension, leaf, &m->padded, &m->depth);
   const int64_t cells = int64_t(1) << (2 * m->depth);
-  m->grid_slot = dev_alloc<int32_t>(cells, ctx->stream);
+  m->grid_slot = dev_alloc<int32_t>(cells, ctx);
   SPG_CUDA(cudaMemsetAsync(m->grid_slot, 0xff, cells * sizeof(int32_t), ctx->stream));
-  m->pyramid = dev_alloc<double>(pyramid_size(m->depth), ctx->stream);
+  m->pyramid = dev_alloc<double>(pyramid_size(m->depth), ctx);
   return m.release();
 }
 
 void finish_matrix(spg_context* ctx, spg_matrix* m, const int32_t* slot_rows,
                    const int32_t* slot_cols, bool check_padding) {
   const int32_t nb_logical = (m->dimension + m->leaf - 1) / m->leaf;
-  DevBuf<double> norms(std::max<int64_t>(m->n_slots, 1), ctx->stream);
-  DevBuf<uint8_t> nonzero(std::max<int64_t>(m->n_slots, 1), ctx->stream);
-  DevBuf<int> bad(1, ctx->stream);
+  DevBuf<double> norms(std::max<int64_t>(m->n_slots, 1), ctx);
+  DevBuf<uint8_t> nonzero(std::max<int64_t>(m->n_slots, 1), ctx);
+  DevBuf<int> bad(1, ctx);
   SPG_CUDA(cudaMemsetAsync(bad.get(), 0, sizeof(int), ctx->stream));
   leaf_norms(ctx, m->payload, m->n_slots, m->leaf, m->dimension, nb_logical,
              check_padding ? slot_rows : nullptr, slot_cols, norms.get(), nonzero.get(),
@@ -173,13 +245,12 @@ __global__ void gather_norms(const uint64_t* __restrict__ keys, int64_t n,
 
 void matrix_destroy(spg_matrix* m) {
   if (!m) return;
-  cudaStream_t s = m->ctx->stream;
-  cudaSetDevice(m->ctx->device);
-  if (m->payload) cudaFreeAsync(m->payload, s);
-  if (m->keys) cudaFreeAsync(m->keys, s);
-  if (m->slots) cudaFreeAsync(m->slots, s);
-  if (m->grid_slot) cudaFreeAsync(m->grid_slot, s);
-  if (m->pyramid) cudaFreeAsync(m->pyramid, s);
+  spg_context* ctx = m->ctx;
+  dev_free(m->payload, ctx);
+  dev_free(m->keys, ctx);
+  dev_free(m->slots, ctx);
+  dev_free(m->grid_slot, ctx);
+  dev_free(m->pyramid, ctx);
   delete m;
 }
 
@@ -190,14 +261,14 @@ spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32
   try {
     m.reset(new_matrix(ctx, dimension, leaf));
   } catch (...) {
-    if (d_payload_owned) cudaFreeAsync(d_payload_owned, ctx->stream);
+    dev_free(d_payload_owned, ctx);
     throw;
   }
   m->payload = d_payload_owned;
   m->n_slots = n_leaves;
   if (n_leaves > (int64_t(1) << 31) - 1) fail(SPG_EINVAL, "too many leaves");
   const int32_t nb_logical = (dimension + leaf - 1) / leaf;
-  DevBuf<int> flags(1, ctx->stream);
+  DevBuf<int> flags(1, ctx);
   SPG_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int), ctx->stream));
   if (n_leaves) {
     scatter_leaves<<<grid_for(n_leaves, 256), 256, 0, ctx->stream>>>(
@@ -221,18 +292,15 @@ spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32
   try {
     m.reset(new_matrix(ctx, dimension, leaf));
   } catch (...) {
-    if (d_payload_owned) cudaFreeAsync(d_payload_owned, ctx->stream);
-    if (d_keys_owned) cudaFreeAsync(d_keys_owned, ctx->stream);
+    dev_free(d_payload_owned, ctx);
+    dev_free(d_keys_owned, ctx);
     throw;
   }
   m->payload = d_payload_owned;
   m->n_slots = n_blocks;
-  DevBuf<uint64_t> keys;
-  keys.p = d_keys_owned;
-  keys.n = n_blocks;
-  keys.s = ctx->stream;
-  DevBuf<int32_t> rows(std::max<int64_t>(n_blocks, 1), ctx->stream);
-  DevBuf<int32_t> cols(std::max<int64_t>(n_blocks, 1), ctx->stream);
+  DevBuf<uint64_t> keys = DevBuf<uint64_t>::adopt(d_keys_owned, n_blocks, ctx);
+  DevBuf<int32_t> rows(std::max<int64_t>(n_blocks, 1), ctx);
+  DevBuf<int32_t> cols(std::max<int64_t>(n_blocks, 1), ctx);
   if (n_blocks) {
     scatter_keys<<<grid_for(n_blocks, 256), 256, 0, ctx->stream>>>(
         d_keys_owned, n_blocks, m->grid_slot, rows.get(), cols.get());
@@ -270,11 +338,6 @@ int spg_context_create(int device, spg_context** out) {
   SPG_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
   SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   for (auto& e : ctx->ev) SPG_CUDA(cudaEventCreate(&e));
-  // Keep freed device memory cached in the pool (stream-ordered allocator).
-  cudaMemPool_t pool;
-  SPG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-  uint64_t threshold = UINT64_MAX;
-  SPG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
   *out = ctx.release();
   SPG_API_END
 }
@@ -284,6 +347,9 @@ int spg_context_destroy(spg_context* ctx) {
   if (!ctx) return SPG_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  ctx->pool.trim(ctx->stream);
+  for (auto& kv : ctx->pool.live) cudaFree(kv.first);
+  ctx->pool.live.clear();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -324,13 +390,10 @@ int spg_matrix_upload(spg_context* ctx, int32_t dimension, int32_t leaf_size, in
   int32_t padded, depth;
   check_shape(dimension, leaf_size, &padded, &depth);
   const int64_t elems = static_cast<int64_t>(leaf_size) * leaf_size;
-  DevBuf<int32_t> rows(std::max<int64_t>(n_leaves, 1), ctx->stream);
-  DevBuf<int32_t> cols(std::max<int64_t>(n_leaves, 1), ctx->stream);
-  double* d_payload = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx->stream);
-  DevBuf<double> payload_guard;
-  payload_guard.p = d_payload;
-  payload_guard.n = 1;
-  payload_guard.s = ctx->stream;
+  DevBuf<int32_t> rows(std::max<int64_t>(n_leaves, 1), ctx);
+  DevBuf<int32_t> cols(std::max<int64_t>(n_leaves, 1), ctx);
+  double* d_payload = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx);
+  DevBuf<double> payload_guard = DevBuf<double>::adopt(d_payload, 1, ctx);
   if (n_leaves) {
     SPG_CUDA(cudaMemcpyAsync(rows.get(), block_rows, n_leaves * sizeof(int32_t),
                              cudaMemcpyHostToDevice, ctx->stream));
@@ -357,7 +420,7 @@ int spg_matrix_upload_device(spg_context* ctx, int32_t dimension, int32_t leaf_s
   int32_t padded, depth;
   check_shape(dimension, leaf_size, &padded, &depth);
   const int64_t elems = static_cast<int64_t>(leaf_size) * leaf_size;
-  double* copy = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx->stream);
+  double* copy = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx);
   if (n_leaves)
     SPG_CUDA(cudaMemcpyAsync(copy, d_payload, n_leaves * elems * sizeof(double),
                              cudaMemcpyDeviceToDevice, ctx->stream));
@@ -433,7 +496,7 @@ int spg_matrix_download(const spg_matrix* m, int32_t* block_rows, int32_t* block
     const int64_t elems = static_cast<int64_t>(m->leaf) * m->leaf;
     // chunked gather + copy keeps the staging buffer bounded
     const int64_t chunk = std::max<int64_t>(1, (int64_t(256) << 20) / (elems * 8));
-    DevBuf<double> stage(std::min(chunk, m->nnzb) * elems, ctx->stream);
+    DevBuf<double> stage(std::min(chunk, m->nnzb) * elems, ctx);
     for (int64_t lo = 0; lo < m->nnzb; lo += chunk) {
       const int64_t n = std::min(chunk, m->nnzb - lo);
       dim3 grid(static_cast<unsigned>(std::min<int64_t>((elems + 255) / 256, 64)),
@@ -447,7 +510,7 @@ int spg_matrix_download(const spg_matrix* m, int32_t* block_rows, int32_t* block
     }
   }
   if (norms) {
-    DevBuf<double> d_norms(m->nnzb, ctx->stream);
+    DevBuf<double> d_norms(m->nnzb, ctx);
     gather_norms<<<grid_for(m->nnzb, 256), 256, 0, ctx->stream>>>(
         m->keys, m->nnzb, m->pyramid + level_offset(m->depth), d_norms.get());
     SPG_CHECK_LAUNCH(ctx);

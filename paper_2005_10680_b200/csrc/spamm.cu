@@ -86,13 +86,15 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
   const int d = a->depth;
   TaskList tl;
   tl.kbits = d;
+  PhaseTrace tr_all(ctx, "tasklist.total");
   TripleList cur = root_list<R>(ctx, a, b, tau);
   DevBuf<uint64_t> keys;
   if (d == 0) {
     tl.n_surv = cur.n;
-    keys = DevBuf<uint64_t>(1, ctx->stream);
+    keys = DevBuf<uint64_t>(1, ctx);
     SPG_CUDA(cudaMemsetAsync(keys.get(), 0, sizeof(uint64_t), ctx->stream));
   } else {
+    PhaseTrace tr(ctx, "tasklist.expand");
     for (int l = 0; l < d - 1 && cur.n > 0; ++l) {
       TripleList next = expand_level<R>(ctx, cur, a->pyramid + level_offset(l + 1),
                                         b->pyramid + level_offset(l + 1), tau);
@@ -100,9 +102,9 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
     }
     // last level: write sort keys directly
     const int64_t n = cur.n;
-    DevBuf<uint8_t> masks(std::max<int64_t>(n, 1), ctx->stream);
-    DevBuf<int64_t> counts(n + 1, ctx->stream);
-    DevBuf<int64_t> offsets(n + 1, ctx->stream);
+    DevBuf<uint8_t> masks(std::max<int64_t>(n, 1), ctx);
+    DevBuf<int64_t> counts(n + 1, ctx);
+    DevBuf<int64_t> offsets(n + 1, ctx);
     SPG_CUDA(cudaMemsetAsync(counts.get() + n, 0, sizeof(int64_t), ctx->stream));
     if (n) {
       expand_count<R><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
@@ -111,7 +113,7 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
       SPG_CHECK_LAUNCH(ctx);
     }
     tl.n_surv = scan_counts(ctx, counts.get(), n, offsets.get());
-    keys = DevBuf<uint64_t>(std::max<int64_t>(tl.n_surv, 1), ctx->stream);
+    keys = DevBuf<uint64_t>(std::max<int64_t>(tl.n_surv, 1), ctx);
     if (tl.n_surv) {
       expand_write_keys<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
           cur.I.get(), cur.K.get(), cur.J.get(), n, masks.get(), offsets.get(), d, keys.get());
@@ -119,12 +121,13 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
     }
   }
   if (tl.n_surv > 1) {
-    DevBuf<uint64_t> sorted(tl.n_surv, ctx->stream);
+    PhaseTrace tr(ctx, "tasklist.sort");
+    DevBuf<uint64_t> sorted(tl.n_surv, ctx);
     size_t bytes = 0;
     const int end_bit = std::max(1, 3 * d);
     SPG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, keys.get(), sorted.get(), tl.n_surv,
                                             0, end_bit, ctx->stream));
-    DevBuf<uint8_t> tmp(bytes, ctx->stream);
+    DevBuf<uint8_t> tmp(bytes, ctx);
     SPG_CUDA(cub::DeviceRadixSort::SortKeys(tmp.get(), bytes, keys.get(), sorted.get(),
                                             tl.n_surv, 0, end_bit, ctx->stream));
     ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
@@ -136,8 +139,8 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
 
 int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix* b) {
   const int nb = 1 << a->depth;
-  DevBuf<int32_t> colA(nb, ctx->stream), rowB(nb, ctx->stream);
-  DevBuf<int64_t> prod(nb, ctx->stream), total(1, ctx->stream);
+  DevBuf<int32_t> colA(nb, ctx), rowB(nb, ctx);
+  DevBuf<int64_t> prod(nb, ctx), total(1, ctx);
   SPG_CUDA(cudaMemsetAsync(colA.get(), 0, nb * sizeof(int32_t), ctx->stream));
   SPG_CUDA(cudaMemsetAsync(rowB.get(), 0, nb * sizeof(int32_t), ctx->stream));
   if (a->nnzb) {
@@ -155,7 +158,7 @@ int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix
   SPG_CHECK_LAUNCH(ctx);
   size_t bytes = 0;
   SPG_CUDA(cub::DeviceReduce::Sum(nullptr, bytes, prod.get(), total.get(), nb, ctx->stream));
-  DevBuf<uint8_t> tmp(bytes, ctx->stream);
+  DevBuf<uint8_t> tmp(bytes, ctx);
   SPG_CUDA(cub::DeviceReduce::Sum(tmp.get(), bytes, prod.get(), total.get(), nb, ctx->stream));
   ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   return copy_scalar_to_host_i64(ctx, total.get());
@@ -178,10 +181,10 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
   if (n_out == 0) return;
   switch (L) {
     case 32:
-      launch_dmma<32, 32, 16, 8, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+      launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C);
       break;
     case 64:
-      launch_dmma<64, 32, 32, 16, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C);
       break;
     case 128:
       launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C);
@@ -213,27 +216,28 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   DevBuf<int64_t> out_offset;
   DevBuf<int2> pairs;
   if (n_surv) {
-    DevBuf<uint8_t> flags(n_surv, ctx->stream);
+    PhaseTrace tr(ctx, "tasklist.group+pairs");
+    DevBuf<uint8_t> flags(n_surv, ctx);
     head_flags<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
                                                               flags.get());
     SPG_CHECK_LAUNCH(ctx);
-    DevBuf<int64_t> heads(n_surv, ctx->stream);
-    DevBuf<int64_t> n_sel(1, ctx->stream);
+    DevBuf<int64_t> heads(n_surv, ctx);
+    DevBuf<int64_t> n_sel(1, ctx);
     thrust::counting_iterator<int64_t> it(0);
     size_t bytes = 0;
     SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags.get(), heads.get(), n_sel.get(),
                                         n_surv, ctx->stream));
-    DevBuf<uint8_t> tmp(bytes, ctx->stream);
+    DevBuf<uint8_t> tmp(bytes, ctx);
     SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flags.get(), heads.get(),
                                         n_sel.get(), n_surv, ctx->stream));
     ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
     n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
-    out_keys = DevBuf<uint64_t>(n_out, ctx->stream);
-    out_offset = DevBuf<int64_t>(n_out + 1, ctx->stream);
+    out_keys = DevBuf<uint64_t>(n_out, ctx);
+    out_offset = DevBuf<int64_t>(n_out + 1, ctx);
     run_outputs<<<grid_for(n_out + 1, 256), 256, 0, ctx->stream>>>(
         tl.keys.get(), heads.get(), n_out, n_surv, tl.kbits, out_keys.get(), out_offset.get());
     SPG_CHECK_LAUNCH(ctx);
-    pairs = DevBuf<int2>(n_surv, ctx->stream);
+    pairs = DevBuf<int2>(n_surv, ctx);
     make_pairs<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
                                                               a->grid_slot, b->grid_slot,
                                                               pairs.get());
@@ -241,13 +245,19 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   }
   tl.keys.reset();
   SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
-  double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx->stream);
+  double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+  {
+  PhaseTrace tr(ctx, "gemm");
   run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload);
+  }
   SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
   pairs.reset();
   out_offset.reset();
-  spg_matrix* c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, out_keys.release(),
-                                            c_payload);
+  spg_matrix* c = nullptr;
+  {
+    PhaseTrace tr(ctx, "finalize");
+    c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, out_keys.release(), c_payload);
+  }
   SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
   SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   if (stats) {

@@ -228,7 +228,7 @@ spg_matrix* device_blocks_to_matrix(spg_context* ctx, int32_t n, int32_t L,
                                     const std::vector<uint64_t>& hkeys, double* payload,
                                     DevBuf<uint64_t>& dkeys) {
   const int64_t nblk = static_cast<int64_t>(hkeys.size());
-  DevBuf<int32_t> r(std::max<int64_t>(nblk, 1), ctx->stream), c(std::max<int64_t>(nblk, 1), ctx->stream);
+  DevBuf<int32_t> r(std::max<int64_t>(nblk, 1), ctx), c(std::max<int64_t>(nblk, 1), ctx);
   if (nblk) {
     keys_to_rc<<<grid_for(nblk, 256), 256, 0, ctx->stream>>>(dkeys.get(), nblk, r.get(), c.get());
     SPG_CHECK_LAUNCH(ctx);
@@ -317,10 +317,10 @@ int spg_synth_chain_device(spg_context* ctx, int32_t n, int32_t L, double ell, u
   }
   const int64_t nblk = static_cast<int64_t>(hkeys.size());
   const int64_t LL = static_cast<int64_t>(L) * L;
-  DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx->stream);
+  DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx);
   SPG_CUDA(cudaMemcpyAsync(dkeys.get(), hkeys.data(), nblk * sizeof(uint64_t),
                            cudaMemcpyHostToDevice, ctx->stream));
-  double* payload = dev_alloc<double>(std::max<int64_t>(nblk * LL, 1), ctx->stream);
+  double* payload = dev_alloc<double>(std::max<int64_t>(nblk * LL, 1), ctx);
   if (nblk) {
     chain_blocks_kernel<<<static_cast<unsigned>(std::min<int64_t>(nblk, 65535)), 256, 0,
                           ctx->stream>>>(dkeys.get(), nblk, n, L, ell, mix64(seed), drop, payload);
@@ -342,11 +342,11 @@ int spg_synth_cluster_device(spg_context* ctx, int32_t n, int32_t L, double ell,
   check_shape(n, L, &padded, &depth);
   CtxGuard g(ctx);
   const std::vector<double> sites = cluster_sites(n / 4, density, site_seed, nullptr);
-  DevBuf<double> dsites(sites.size(), ctx->stream);
+  DevBuf<double> dsites(sites.size(), ctx);
   SPG_CUDA(cudaMemcpyAsync(dsites.get(), sites.data(), sites.size() * sizeof(double),
                            cudaMemcpyHostToDevice, ctx->stream));
   const uint64_t sm = mix64(value_seed);
-  DevBuf<double> rowsum(n, ctx->stream), scale(1, ctx->stream);
+  DevBuf<double> rowsum(n, ctx), scale(1, ctx);
   cluster_rowsum_kernel<<<grid_for(int64_t(n) * 32, 256), 256, 0, ctx->stream>>>(
       dsites.get(), n, ell, sm, rowsum.get());
   SPG_CHECK_LAUNCH(ctx);
@@ -356,10 +356,10 @@ int spg_synth_cluster_device(spg_context* ctx, int32_t n, int32_t L, double ell,
   const std::vector<uint64_t> hkeys = morton_blocks(nb, depth);
   const int64_t nblk = static_cast<int64_t>(hkeys.size());
   const int64_t LL = static_cast<int64_t>(L) * L;
-  DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx->stream);
+  DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx);
   SPG_CUDA(cudaMemcpyAsync(dkeys.get(), hkeys.data(), nblk * sizeof(uint64_t),
                            cudaMemcpyHostToDevice, ctx->stream));
-  double* payload = dev_alloc<double>(std::max<int64_t>(nblk * LL, 1), ctx->stream);
+  double* payload = dev_alloc<double>(std::max<int64_t>(nblk * LL, 1), ctx);
   if (nblk) {
     cluster_blocks_kernel<<<static_cast<unsigned>(std::min<int64_t>(nblk, 1 << 20)), 256, 0,
                             ctx->stream>>>(dkeys.get(), nblk, dsites.get(), n, L, ell, sm,

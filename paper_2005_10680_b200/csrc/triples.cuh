@@ -102,7 +102,7 @@ static __global__ void expand_write_keys(const int32_t* __restrict__ I, const in
 inline int64_t scan_counts(spg_context* ctx, const int64_t* counts, int64_t n, int64_t* offsets) {
   size_t bytes = 0;
   SPG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, counts, offsets, n + 1, ctx->stream));
-  DevBuf<uint8_t> tmp(bytes, ctx->stream);
+  DevBuf<uint8_t> tmp(bytes, ctx);
   SPG_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), bytes, counts, offsets, n + 1, ctx->stream));
   ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   int64_t total = 0;
@@ -119,9 +119,9 @@ TripleList expand_level(spg_context* ctx, TripleList& parent, const double* pa_c
                         const double* pb_child_level, double tau) {
   TripleList out;
   const int64_t n = parent.n;
-  DevBuf<uint8_t> masks(std::max<int64_t>(n, 1), ctx->stream);
-  DevBuf<int64_t> counts(n + 1, ctx->stream);
-  parent.child_offset = DevBuf<int64_t>(n + 1, ctx->stream);
+  DevBuf<uint8_t> masks(std::max<int64_t>(n, 1), ctx);
+  DevBuf<int64_t> counts(n + 1, ctx);
+  parent.child_offset = DevBuf<int64_t>(n + 1, ctx);
   SPG_CUDA(cudaMemsetAsync(counts.get() + n, 0, sizeof(int64_t), ctx->stream));
   if (n) {
     expand_count<R><<<grid_for(n, 256), 256, 0, ctx->stream>>>(
@@ -131,9 +131,9 @@ TripleList expand_level(spg_context* ctx, TripleList& parent, const double* pa_c
   }
   const int64_t total = scan_counts(ctx, counts.get(), n, parent.child_offset.get());
   out.n = total;
-  out.I = DevBuf<int32_t>(std::max<int64_t>(total, 1), ctx->stream);
-  out.K = DevBuf<int32_t>(std::max<int64_t>(total, 1), ctx->stream);
-  out.J = DevBuf<int32_t>(std::max<int64_t>(total, 1), ctx->stream);
+  out.I = DevBuf<int32_t>(std::max<int64_t>(total, 1), ctx);
+  out.K = DevBuf<int32_t>(std::max<int64_t>(total, 1), ctx);
+  out.J = DevBuf<int32_t>(std::max<int64_t>(total, 1), ctx);
   if (total) {
     expand_write<<<grid_for(n, 256), 256, 0, ctx->stream>>>(
         parent.I.get(), parent.K.get(), parent.J.get(), n, masks.get(),
@@ -157,9 +157,9 @@ TripleList root_list(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
   }
   TripleList out;
   out.n = keep ? 1 : 0;
-  out.I = DevBuf<int32_t>(1, ctx->stream);
-  out.K = DevBuf<int32_t>(1, ctx->stream);
-  out.J = DevBuf<int32_t>(1, ctx->stream);
+  out.I = DevBuf<int32_t>(1, ctx);
+  out.K = DevBuf<int32_t>(1, ctx);
+  out.J = DevBuf<int32_t>(1, ctx);
   SPG_CUDA(cudaMemsetAsync(out.I.get(), 0, sizeof(int32_t), ctx->stream));
   SPG_CUDA(cudaMemsetAsync(out.K.get(), 0, sizeof(int32_t), ctx->stream));
   SPG_CUDA(cudaMemsetAsync(out.J.get(), 0, sizeof(int32_t), ctx->stream));
