@@ -146,6 +146,28 @@ int spg_spamm_with_error_control(spg_context* ctx, const spg_matrix* a, const sp
 int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                   int64_t* count, int32_t* triples, int64_t capacity);
 
+/* ---- row shards across GPUs (new, the reference is single-
+ * process) --------------------------------------------------------------
+ * A shard at `level` s owns output block-rows [shard*nb/2^s, (shard+1)*nb/2^s)
+ * (power-of-two aligned), shard in [0, 2^s).  Bounds assembled from all
+ * shards are bit-identical to spg_cse; the union of the shard products is
+ * spg_spamm's C, block for block. */
+/* The shard's level-s partial bound vectors: 4^s x n_taus doubles, vector of
+ * pair (shard, K, J) at index (K * 2^s + J) * n_taus; zeros for null pairs. */
+int spg_cse_shard(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, const double* taus,
+                  int32_t n_taus, int32_t level, int32_t shard, double* partial);
+/* Host-only: combine the gathered partials (2^s shards in order, each as
+ * above) through the top s levels in reference order (cse_node,
+ * error_control.cpp:46-79).  a/b_top_norms: node norms of levels 0..s-1,
+ * concatenated Morton grids (spg_matrix_top_norms). */
+int spg_cse_finish(int32_t level, const double* a_top_norms, const double* b_top_norms,
+                   int32_t n_taus, const double* partials, double* bounds);
+/* Concatenated Morton norm grids of levels 0..levels-1 ((4^levels-1)/3 doubles). */
+int spg_matrix_top_norms(const spg_matrix* m, int32_t levels, double* out);
+/* spamm_multiply restricted to the shard's output block-rows. */
+int spg_spamm_shard(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                    int32_t level, int32_t shard, spg_matrix** c, spg_spamm_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,8 @@ class Oracle:
         self._spamm = fn("spamm", _vp, [_vp, _vp, C.c_double, C.POINTER(C.c_int)])
         self._exact = fn("multiply_exact", _vp, [_vp, _vp, C.POINTER(C.c_int)])
         self._surv = fn("survivors", C.c_int64, [_vp, _vp, C.c_double, _i32p, C.c_int64])
+        self._cse_sub = fn("cse_subtree", C.c_int, [_vp, _vp, _dp, C.c_int, C.c_int, C.c_int32,
+                                                   C.c_int32, C.c_int32, _dp])
         if kind == "port":
             self._select = fn("select_index", C.c_int, [_dp, C.c_int, C.c_double])
             self._cand = fn("candidates", C.c_int64, [_vp, _vp])
@@ -156,6 +158,20 @@ class Oracle:
         if self._cse(a.h, b.h, _p(taus, C.c_double), taus.size, _p(out, C.c_double)) != 0:
             raise ValueError("cse: dimension or leaf size mismatch")
         return out
+
+    def cse_subtree(self, a: Tree, b: Tree, taus, level: int, I: int, K: int, J: int):
+        taus = np.ascontiguousarray(taus, np.float64)
+        out = np.empty(taus.size)
+        if self._cse_sub(a.h, b.h, _p(taus, C.c_double), taus.size, level, I, K, J,
+                         _p(out, C.c_double)) != 0:
+            raise ValueError("cse_subtree: invalid arguments")
+        return out
+
+    def shard_partials(self, a: Tree, b: Tree, taus, level: int, shard: int) -> np.ndarray:
+        """What spg_cse_shard returns, from the oracle: (4^level, n_taus)."""
+        side = 2 ** level
+        return np.stack([self.cse_subtree(a, b, taus, level, shard, K, J)
+                         for K in range(side) for J in range(side)])
 
     @staticmethod
     def select_index(bounds, delta: float) -> int:

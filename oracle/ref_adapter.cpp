@@ -228,6 +228,29 @@ int ref_cse(const void* a, const void* b, const double* taus, int n, double* bou
   }
 }
 
+// cse_node for the pair A(I,K) x B(K,J) at `level`: spamm::cse on the two
+// subtrees wrapped as matrices of the subtree size (same recursion).
+int ref_cse_subtree(const void* a, const void* b, const double* taus, int n, int level,
+                    std::int32_t I, std::int32_t K, std::int32_t J, double* out) {
+  try {
+    const auto* ra = static_cast<const RefTree*>(a);
+    const auto* rb = static_cast<const RefTree*>(b);
+    auto at = [&](NodePtr nd, std::int32_t r, std::int32_t c) {
+      for (int l = level - 1; l >= 0 && nd; --l) nd = nd->child[2 * ((r >> l) & 1) + ((c >> l) & 1)];
+      return nd;
+    };
+    const int size = ra->m.padded_dimension() >> level;
+    const auto sa = QuadTreeMatrix::wrap(at(ra->m.root(), I, K), size, ra->m.leaf_size());
+    const auto sb = QuadTreeMatrix::wrap(at(rb->m.root(), K, J), size, rb->m.leaf_size());
+    const spamm::ToleranceGrid grid(std::vector<double>(taus, taus + n));
+    const auto e = spamm::cse(sa, sb, grid);
+    std::memcpy(out, e.bounds.data(), sizeof(double) * n);
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
 // spamm::select_tolerance (error_control.cpp:168-172); returns tau (0 = exact).
 double ref_select_tolerance(const double* bounds, const double* taus, int n, double delta) {
   const spamm::ToleranceGrid grid(std::vector<double>(taus, taus + n));

@@ -321,6 +321,22 @@ int ora_cse(const ora_tree* a, const ora_tree* b, const double* taus, int n_taus
   return 0;
 }
 
+static const ora_node* node_at(const ora_node* n, int level, int32_t r, int32_t c) {
+  for (int l = level - 1; l >= 0 && n; --l) n = n->child[2 * ((r >> l) & 1) + ((c >> l) & 1)];
+  return n;
+}
+
+int ora_cse_subtree(const ora_tree* a, const ora_tree* b, const double* taus, int n_taus, int level,
+                    int32_t I, int32_t K, int32_t J, double* out) {
+  if (!conformable(a, b) || n_taus < 1 || level < 0 || level > a->depth) return -1;
+  cse_ctx cx = {taus, n_taus, a->depth, NULL};
+  cx.scratch = (double*)malloc(sizeof(double) * 5 * (size_t)n_taus * (size_t)(a->depth + 1));
+  memset(out, 0, sizeof(double) * (size_t)n_taus);
+  cse_node(&cx, node_at(a->root, level, I, K), node_at(b->root, level, K, J), level, out);
+  free(cx.scratch);
+  return 0;
+}
+
 /* select_index: error_control.cpp:81-87. */
 int ora_select_index(const double* bounds, int n_taus, double delta) {
   for (int k = 0; k < n_taus; ++k)

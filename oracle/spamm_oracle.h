@@ -61,6 +61,11 @@ void ora_level_norms(const ora_tree* t, int level, double* out);
 /* CSE sweep (error_control.cpp:34-79,160-166). Returns 0, or -1 on mismatch. */
 int ora_cse(const ora_tree* a, const ora_tree* b, const double* taus, int n_taus, double* bounds);
 
+/* cse_node (error_control.cpp:46-79) for the pair A(I,K) x B(K,J) at `level`
+ * (the partial vector a row shard contributes). */
+int ora_cse_subtree(const ora_tree* a, const ora_tree* b, const double* taus, int n_taus, int level,
+                    int32_t I, int32_t K, int32_t J, double* out);
+
 /* First k with bounds[k] < delta (error_control.cpp:81-87); -1 if none. */
 int ora_select_index(const double* bounds, int n_taus, double delta);
 

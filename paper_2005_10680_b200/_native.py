@@ -94,6 +94,11 @@ _SIGNATURES = {
     "spg_spamm_with_error_control": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
                                                C.POINTER(_vp), _dp, C.POINTER(ControlledStats)]),
     "spg_survivors": (C.c_int, [_vp, _vp, _vp, C.c_double, _i64p, _i32p, C.c_int64]),
+    "spg_cse_shard": (C.c_int, [_vp, _vp, _vp, _dp, C.c_int32, C.c_int32, C.c_int32, _dp]),
+    "spg_cse_finish": (C.c_int, [C.c_int32, _dp, _dp, C.c_int32, _dp, _dp]),
+    "spg_matrix_top_norms": (C.c_int, [_vp, C.c_int32, _dp]),
+    "spg_spamm_shard": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32,
+                                  C.POINTER(_vp), C.POINTER(SpammStats)]),
     "spg_synth_chain_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double,
                                        C.c_int64, _i32p, _i32p, _dp, _i64p]),
     "spg_synth_cluster_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
@@ -358,6 +363,44 @@ def survivors(ctx: Context, a: Matrix, b: Matrix, tau: float) -> np.ndarray:
         _check(lib().spg_survivors(ctx.handle, a.handle, b.handle, tau, C.byref(count),
                                    _ptr(out, C.c_int32), count.value))
     return out
+
+
+# ---------------------------------------------------------------- row shards
+def cse_shard(ctx: Context, a: Matrix, b: Matrix, taus, level: int, shard: int) -> np.ndarray:
+    """Level-`level` partial bound vectors of one row shard: (4^level, n_taus)."""
+    taus = np.ascontiguousarray(taus, np.float64)
+    out = np.empty((4 ** level, taus.size), np.float64)
+    _check(lib().spg_cse_shard(ctx.handle, a.handle, b.handle, _ptr(taus, C.c_double), taus.size,
+                               level, shard, _ptr(out, C.c_double)))
+    return out
+
+
+def cse_finish(level: int, a_top, b_top, partials) -> np.ndarray:
+    """Host-only top-level combine of gathered partials (2^level shards)."""
+    a_top = np.ascontiguousarray(a_top, np.float64)
+    b_top = np.ascontiguousarray(b_top, np.float64)
+    partials = np.ascontiguousarray(partials, np.float64)
+    n_taus = partials.shape[-1]
+    if partials.size != (2 ** level) * (4 ** level) * n_taus:
+        raise ValueError("partials must hold 2^level shards x 4^level vectors")
+    out = np.empty(n_taus, np.float64)
+    _check(lib().spg_cse_finish(level, _ptr(a_top, C.c_double), _ptr(b_top, C.c_double), n_taus,
+                                _ptr(partials, C.c_double), _ptr(out, C.c_double)))
+    return out
+
+
+def top_norms(m: Matrix, levels: int) -> np.ndarray:
+    out = np.empty(((4 ** levels) - 1) // 3, np.float64)
+    _check(lib().spg_matrix_top_norms(m.handle, levels, _ptr(out, C.c_double)))
+    return out
+
+
+def spamm_shard(ctx: Context, a: Matrix, b: Matrix, tau: float, level: int, shard: int):
+    h = _vp()
+    st = SpammStats()
+    _check(lib().spg_spamm_shard(ctx.handle, a.handle, b.handle, tau, level, shard, C.byref(h),
+                                 C.byref(st)))
+    return Matrix(ctx, h), st.as_dict()
 
 
 # ---------------------------------------------------------------- synthetic inputs

@@ -198,12 +198,18 @@ spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32
                                       double* d_payload_owned);
 void matrix_destroy(spg_matrix* m);
 void check_shape(int32_t dimension, int32_t leaf, int32_t* padded, int32_t* depth);
-// cse.cu
+// Row shard of a product: level 0 = the whole matrix.
+struct Shard {
+  int level = 0;
+  int index = 0;
+};
+// cse.cu -- with shard.level > 0, `out` receives the level-s partial bound
+// vectors of the shard (4^level x n_taus, dense (K, J) order) instead of bounds
 void cse_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, const double* taus,
-                int n_taus, double* bounds_host, float* ms);
+                int n_taus, double* out, float* ms, Shard shard = {});
 // spamm.cu
 spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
-                         bool skip_test, spg_spamm_stats* stats);
+                         bool skip_test, spg_spamm_stats* stats, Shard shard = {});
 
 int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
 

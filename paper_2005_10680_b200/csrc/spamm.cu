@@ -80,22 +80,39 @@ struct TaskList {
   int kbits = 0;
 };
 
-// Surviving (i,k,j) leaf products, sorted by (Morton(i,j), k).
+__global__ void triples_to_keys(const int32_t* __restrict__ I, const int32_t* __restrict__ K,
+                                const int32_t* __restrict__ J, int64_t n, int kbits,
+                                uint64_t* __restrict__ keys) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  keys[t] = (morton2(static_cast<uint32_t>(I[t]), static_cast<uint32_t>(J[t])) << kbits) |
+            static_cast<uint32_t>(K[t]);
+}
+
+// Surviving (i,k,j) leaf products, sorted by (Morton(i,j), k); with a shard,
+// only the leaf products of its block-rows (ancestors above the shard level
+// are tested on the host, shard_list).
 template <KeepRule R>
-TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau) {
+TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                        Shard sh) {
   const int d = a->depth;
   TaskList tl;
   tl.kbits = d;
   PhaseTrace tr_all(ctx, "tasklist.total");
-  TripleList cur = root_list<R>(ctx, a, b, tau);
+  TripleList cur = sh.level == 0 ? root_list<R>(ctx, a, b, tau)
+                                 : shard_list<R>(ctx, a, b, sh.level, sh.index, tau, true);
   DevBuf<uint64_t> keys;
-  if (d == 0) {
+  if (sh.level == d) {
     tl.n_surv = cur.n;
-    keys = DevBuf<uint64_t>(1, ctx);
-    SPG_CUDA(cudaMemsetAsync(keys.get(), 0, sizeof(uint64_t), ctx->stream));
+    keys = DevBuf<uint64_t>(std::max<int64_t>(cur.n, 1), ctx);
+    if (cur.n) {
+      triples_to_keys<<<grid_for(cur.n, 256), 256, 0, ctx->stream>>>(
+          cur.I.get(), cur.K.get(), cur.J.get(), cur.n, d, keys.get());
+      SPG_CHECK_LAUNCH(ctx);
+    }
   } else {
     PhaseTrace tr(ctx, "tasklist.expand");
-    for (int l = 0; l < d - 1 && cur.n > 0; ++l) {
+    for (int l = sh.level; l < d - 1 && cur.n > 0; ++l) {
       TripleList next = expand_level<R>(ctx, cur, a->pyramid + level_offset(l + 1),
                                         b->pyramid + level_offset(l + 1), tau);
       cur = std::move(next);
@@ -200,15 +217,18 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
 }  // namespace
 
 spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
-                         bool skip_test, spg_spamm_stats* stats) {
+                         bool skip_test, spg_spamm_stats* stats, Shard shard) {
   if (a->dimension != b->dimension || a->leaf != b->leaf)
     fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
   if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
+  if (shard.level < 0 || shard.level > a->depth || shard.index < 0 ||
+      shard.index >= (1 << shard.level))
+    fail(SPG_EINVAL, "spamm: shard outside the quadtree");
   const int L = a->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau)
-                          : build_tasklist<KeepRule::kExact>(ctx, a, b, tau);
+  TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard)
+                          : build_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard);
   const int64_t n_surv = tl.n_surv;
   // group by output block
   int64_t n_out = 0;
@@ -345,6 +365,16 @@ int spg_spamm_with_error_control(spg_context* ctx, const spg_matrix* a, const sp
   SPG_API_END
 }
 
+int spg_spamm_shard(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                    int32_t level, int32_t shard, spg_matrix** c, spg_spamm_stats* stats) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !c) fail(SPG_EINVAL, "null argument");
+  *c = nullptr;
+  CtxGuard g(ctx);
+  *c = spamm_device(ctx, a, b, tau, true, stats, Shard{level, shard});
+  SPG_API_END
+}
+
 int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                   int64_t* count, int32_t* triples, int64_t capacity) {
   SPG_API_BEGIN
@@ -353,7 +383,7 @@ int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
     fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
   if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
   CtxGuard g(ctx);
-  TaskList tl = build_tasklist<KeepRule::kSkip>(ctx, a, b, tau);
+  TaskList tl = build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, Shard{});
   *count = tl.n_surv;
   if (triples && capacity > 0 && tl.n_surv > 0) {
     const int64_t n = std::min(capacity, tl.n_surv);

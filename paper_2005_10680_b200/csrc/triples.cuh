@@ -166,4 +166,56 @@ TripleList root_list(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
   return out;
 }
 
+// The level-`level` pairs (shard, K, J) of one row shard:
+// block-rows [shard * nb / 2^level, (shard+1) * nb / 2^level) of C.  For the
+// products every ancestor pair must pass the rule too (the reference prunes
+// top-down); the sweep keeps pairs whose own norms pass and lets
+// spg_cse_finish apply the ancestors' masks.
+template <KeepRule R>
+TripleList shard_list(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, int level,
+                      int shard, double tau, bool check_ancestors) {
+  const int64_t top = level_offset(level + 1);
+  std::vector<double> pa(static_cast<size_t>(top)), pb(static_cast<size_t>(top));
+  SPG_CUDA(cudaMemcpyAsync(pa.data(), a->pyramid, top * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaMemcpyAsync(pb.data(), b->pyramid, top * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  auto keep = [&](int l, uint32_t I, uint32_t K, uint32_t J) {
+    const double na = pa[level_offset(l) + morton2(I, K)];
+    const double nb = pb[level_offset(l) + morton2(K, J)];
+    if (na < 0.0 || nb < 0.0) return false;
+    if (R == KeepRule::kExact) return true;
+    volatile double p = na * nb;
+    return R == KeepRule::kSweep ? (p != 0.0) : !(p < tau);
+  };
+  std::vector<int32_t> hI, hK, hJ;
+  const uint32_t side = 1u << level;
+  for (uint32_t K = 0; K < side; ++K)
+    for (uint32_t J = 0; J < side; ++J) {
+      bool ok = keep(level, shard, K, J);
+      for (int l = level - 1; ok && check_ancestors && l >= 0; --l) {
+        const int sh = level - l;
+        ok = keep(l, static_cast<uint32_t>(shard) >> sh, K >> sh, J >> sh);
+      }
+      if (!ok) continue;
+      hI.push_back(shard);
+      hK.push_back(static_cast<int32_t>(K));
+      hJ.push_back(static_cast<int32_t>(J));
+    }
+  TripleList out;
+  out.n = static_cast<int64_t>(hI.size());
+  const size_t cap = std::max<size_t>(hI.size(), 1);
+  out.I = DevBuf<int32_t>(cap, ctx);
+  out.K = DevBuf<int32_t>(cap, ctx);
+  out.J = DevBuf<int32_t>(cap, ctx);
+  if (out.n) {
+    SPG_CUDA(cudaMemcpyAsync(out.I.get(), hI.data(), out.n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(out.K.get(), hK.data(), out.n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(out.J.get(), hJ.data(), out.n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return out;
+}
+
 }  // namespace spg
