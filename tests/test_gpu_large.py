@@ -1,0 +1,119 @@
+"""GPU parity at BASELINE.json's full configs[1] size (cfg2: N=32768, L=64,
+262,048 leaves, 1.34e8 candidate products).  The reference cannot run the
+whole product on CPU in test time, so this checks:
+  * every leaf norm and every level of the norm pyramid, bit for bit, against
+    the reference rule applied on the host to the downloaded payload;
+  * the full bound vector, tau and the survivor count against the reference
+    sweep/recursion on norm-only trees (8c(i));
+  * one block-row of C~ against the reference spamm_multiply restricted to
+    that row (8c(ii)), 1e-12 relative Frobenius;
+  * ||C~ - A*A||_F < delta with A*A from the GPU exact product, itself checked
+    against cuBLAS DGEMM on the dense matrices (8c(iii))."""
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def cfg2(ctx):
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import CONFIGS, log_grid
+    w = CONFIGS["cfg2"]
+    A = nat.synth_cluster_device(ctx, w.n, w.leaf, w.ell, w.density, w.site_seed, w.value_seed,
+                                 w.drop)
+    rows, cols, pay, norms = A.download(payload=True)
+    taus = log_grid(w.n_taus)
+    C, st, bounds = nat.spamm_with_error_control(ctx, A, A, w.delta, taus)
+    return dict(w=w, A=A, rows=rows, cols=cols, pay=pay, norms=norms, taus=taus, C=C, st=st,
+                bounds=bounds)
+
+
+def _oracle():
+    import oracle
+    if oracle.available("ref"):
+        R = oracle.Oracle("ref")
+        import os
+        R.set_threads(os.cpu_count() or 1)
+        return R
+    return oracle.Oracle("port")
+
+
+def test_cfg2_every_norm_bitwise(cfg2, port):
+    import ctypes as C
+    lib = port.L
+    lib.ora_block_norm.restype = C.c_double
+    lib.ora_block_norm.argtypes = [C.POINTER(C.c_double), C.c_int64]
+    pay = cfg2["pay"]
+    want = np.empty(len(pay))
+    LL = pay.shape[1]
+    base = pay.ctypes.data
+    for i in range(len(pay)):  # node_ops.hpp:24-28 on every leaf
+        want[i] = lib.ora_block_norm(C.cast(base + i * LL * 8, C.POINTER(C.c_double)), LL)
+    assert bits_equal(cfg2["norms"], want)
+    t = port.build_norm_only(cfg2["w"].n, cfg2["w"].leaf, cfg2["rows"], cfg2["cols"], want)
+    for lvl in range(t.depth() + 1):
+        assert bits_equal(cfg2["A"].level_norms(lvl), t.level_norms(lvl)), lvl
+
+
+def test_cfg2_bounds_tau_survivors_vs_reference(cfg2):
+    R = _oracle()
+    w = cfg2["w"]
+    t = R.build_norm_only(w.n, w.leaf, cfg2["rows"], cfg2["cols"], cfg2["norms"])
+    bounds = R.cse(t, t, cfg2["taus"])
+    assert bits_equal(cfg2["bounds"], bounds)
+    k = R.select_index(bounds, w.delta)
+    assert k == cfg2["st"]["tau_index"]
+    tau = float(cfg2["taus"][k])
+    assert tau == cfg2["st"]["tau"]
+    assert R._surv(t.h, t.h, tau, None, 0) == cfg2["st"]["spamm"]["survivors"]
+
+
+def test_cfg2_sampled_block_row_vs_reference(cfg2):
+    R = _oracle()
+    w = cfg2["w"]
+    rows, cols, pay = cfg2["rows"], cfg2["cols"], cfg2["pay"]
+    full = R.build(w.n, w.leaf, rows, cols, pay)
+    sel = rows == 137
+    part = R.build(w.n, w.leaf, rows[sel], cols[sel], pay[sel])
+    ref = R.spamm(part, full, cfg2["st"]["tau"])
+    rr, rc, rp, rn = ref.leaves()
+    gr, gc, gp, gn = cfg2["C"].download()
+    mine = gr == 137
+    assert np.array_equal(gr[mine], rr) and np.array_equal(gc[mine], rc)
+    err = np.linalg.norm(gp[mine] - rp) / np.linalg.norm(rp)
+    assert err < 1e-12, err
+
+
+def test_cfg2_delta_bound_against_exact_and_cublas(cfg2, ctx):
+    import torch
+    from paper_2005_10680_b200 import _native as nat
+    w = cfg2["w"]
+    E, _ = nat.multiply_exact(ctx, cfg2["A"], cfg2["A"])
+    er, ec, ep, _ = E.download()
+    ar, ac, ap, _ = cfg2["C"].download()
+    nb = w.n // w.leaf
+    key_e = er.astype(np.int64) * nb + ec
+    key_a = ar.astype(np.int64) * nb + ac
+    order = np.argsort(key_e)
+    idx = order[np.searchsorted(key_e[order], key_a)]
+    diff = ep.copy()
+    diff[idx] -= ap
+    realized = float(np.sqrt(np.sum(diff * diff)))
+    assert realized < w.delta
+    assert realized <= cfg2["st"]["bound"] * (1 + 1e-9)
+    # the exact product against cuBLAS DGEMM on the dense matrices
+    dev = torch.device("cuda", 0)
+    def dense(r, c, p):
+        t = torch.from_numpy(p.reshape(-1, w.leaf, w.leaf)).to(dev)  # [blk, col, row]
+        D = torch.zeros((nb, nb, w.leaf, w.leaf), dtype=torch.float64, device=dev)
+        D[torch.from_numpy(r.astype(np.int64)).to(dev), torch.from_numpy(c.astype(np.int64)).to(dev)] = t.transpose(1, 2)
+        return D.permute(0, 2, 1, 3).reshape(w.n, w.n)
+    Ad = dense(cfg2["rows"], cfg2["cols"], cfg2["pay"])
+    ref = Ad @ Ad
+    del Ad
+    Ed = dense(er, ec, ep)
+    rel = float(torch.linalg.norm(Ed - ref) / torch.linalg.norm(ref))
+    assert rel < 1e-12, rel
