@@ -15,6 +15,7 @@
 // >= 1 survivor; its norm follows block_norm (K1); all-zero sums collapse to
 // null (make_leaf); inner norms follow combine_child_norms (K2).
 #include <chrono>
+#include <cstdlib>
 
 #include <thrust/iterator/counting_iterator.h>
 
@@ -193,9 +194,56 @@ void launch_dmma(spg_context* ctx, const double* A, const double* B, const int2*
   SPG_CHECK_LAUNCH(ctx);
 }
 
+template <int NSTAGE>
+void launch_tma64(spg_context* ctx, const double* A, const double* B, const int2* pairs,
+                  const int64_t* out_offset, int64_t n_out, double* C) {
+  using Cfg = TmaGemmCfg<NSTAGE>;
+  auto kern = leaf_gemm_tma64<NSTAGE>;
+  SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::kSmemBytes)));
+  int per_sm = 1;
+  SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads,
+                                                         Cfg::kSmemBytes));
+  const int64_t grid = std::min<int64_t>(n_out, static_cast<int64_t>(ctx->sm_count) *
+                                                    std::max(per_sm, 1));
+  DevBuf<unsigned long long> counter(1, ctx);
+  SPG_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), ctx->stream));
+  kern<<<static_cast<unsigned>(grid), Cfg::kThreads, Cfg::kSmemBytes, ctx->stream>>>(
+      A, B, pairs, out_offset, n_out, C, counter.get());
+  SPG_CHECK_LAUNCH(ctx);
+}
+
+int gemm_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("SPG_GEMM");  // developer switch: 2 = cp.async kernel
+    return e ? std::atoi(e) : 5;
+  }();
+  return v;
+}
+
 void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const int2* pairs,
               const int64_t* out_offset, int64_t n_out, double* C) {
   if (n_out == 0) return;
+  if (L == 64 && gemm_variant() == 3) {
+    launch_tma64<3>(ctx, A, B, pairs, out_offset, n_out, C);
+    return;
+  }
+  if (L == 64 && gemm_variant() == 4) {  // 4 warps x 32x32, 2 stages, 3 CTAs/SM
+    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C);
+    return;
+  }
+  if (L == 64 && gemm_variant() == 5) {  // 4 warps x 32x32, 3 stages, 2 CTAs/SM
+    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C);
+    return;
+  }
+  if (L == 64 && gemm_variant() == 6) {  // 4 warps x 32x32, KC=16, 4 stages, 3 CTAs/SM
+    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+    return;
+  }
+  if (L == 64 && gemm_variant() == 7) {  // 4 warps x 32x32, KC=16, 6 stages, 2 CTAs/SM
+    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C);
+    return;
+  }
   switch (L) {
     case 32:
       launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C);
