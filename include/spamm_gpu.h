@@ -140,6 +140,17 @@ int spg_multiply_exact(spg_context* ctx, const spg_matrix* a, const spg_matrix* 
 int spg_spamm_with_error_control(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
                                  double delta, const double* taus, int32_t n_taus,
                                  spg_matrix** c, double* bounds, spg_controlled_stats* stats);
+/* spg_spamm_with_error_control with C delivered to host buffers: the leaf
+ * GEMM runs in chunks and each finished chunk is copied D2H while the next
+ * one computes (use pinned buffers for the overlap).  Outputs equal
+ * spg_spamm_with_error_control + spg_matrix_download: *c_count non-null
+ * leaves in Morton order (capacity >= number of output blocks). */
+int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
+                                         const spg_matrix* b, double delta, const double* taus,
+                                         int32_t n_taus, int64_t capacity, int32_t* c_rows,
+                                         int32_t* c_cols, double* c_payload, double* c_norms,
+                                         int64_t* c_count, double* bounds,
+                                         spg_controlled_stats* stats);
 /* The surviving leaf-product set of spamm_multiply(a, b, tau) (the leaves the
  * recursion of multiply.cpp:70-92 reaches) as (i, k, j) block triples sorted
  * by (Morton(i, j), k).  Writes min(count, capacity) triples. */

@@ -94,6 +94,9 @@ _SIGNATURES = {
     "spg_spamm_with_error_control": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
                                                C.POINTER(_vp), _dp, C.POINTER(ControlledStats)]),
     "spg_survivors": (C.c_int, [_vp, _vp, _vp, C.c_double, _i64p, _i32p, C.c_int64]),
+    "spg_spamm_with_error_control_to_host": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
+                                                       C.c_int64, _i32p, _i32p, _dp, _dp, _i64p,
+                                                       _dp, C.POINTER(ControlledStats)]),
     "spg_cse_shard": (C.c_int, [_vp, _vp, _vp, _dp, C.c_int32, C.c_int32, C.c_int32, _dp]),
     "spg_cse_finish": (C.c_int, [C.c_int32, _dp, _dp, C.c_int32, _dp, _dp]),
     "spg_matrix_top_norms": (C.c_int, [_vp, C.c_int32, _dp]),
@@ -194,7 +197,7 @@ class Context:
     def __del__(self):
         # At interpreter exit the CUDA runtime may already be torn down;
         # leaking device memory then is harmless, calling into it is not.
-        if sys.is_finalizing():
+        if sys is None or sys.is_finalizing():
             return
         try:
             self.close()
@@ -264,7 +267,7 @@ class Matrix:
             self._h = None
 
     def __del__(self):
-        if sys.is_finalizing():
+        if sys is None or sys.is_finalizing():
             return
         try:
             self.free()
@@ -353,6 +356,29 @@ def spamm_with_error_control(ctx: Context, a: Matrix, b: Matrix, delta: float, t
                                               _ptr(taus, C.c_double), taus.size, C.byref(h),
                                               _ptr(bounds, C.c_double), C.byref(st)))
     return Matrix(ctx, h), st.as_dict(), bounds
+
+
+def spamm_with_error_control_to_host(ctx: Context, a: Matrix, b: Matrix, delta: float, taus,
+                                     out=None):
+    """Controlled product with C streamed to host arrays (rows, cols, payload,
+    norms); `out` may supply (pinned) preallocated arrays of capacity n."""
+    taus = np.ascontiguousarray(taus, np.float64)
+    inf = a.info()
+    if out is None:
+        nb = (inf.dimension + inf.leaf_size - 1) // inf.leaf_size
+        cap = nb * nb
+        out = (np.empty(cap, np.int32), np.empty(cap, np.int32),
+               np.empty((cap, inf.leaf_size * inf.leaf_size)), np.empty(cap))
+    rows, cols, pay, norms = out
+    count = C.c_int64(0)
+    bounds = np.empty(taus.size)
+    st = ControlledStats()
+    _check(lib().spg_spamm_with_error_control_to_host(
+        ctx.handle, a.handle, b.handle, delta, _ptr(taus, C.c_double), taus.size, len(rows),
+        _ptr(rows, C.c_int32), _ptr(cols, C.c_int32), _ptr(pay, C.c_double),
+        _ptr(norms, C.c_double), C.byref(count), _ptr(bounds, C.c_double), C.byref(st)))
+    n = count.value
+    return (rows[:n], cols[:n], pay[:n], norms[:n]), st.as_dict(), bounds
 
 
 def survivors(ctx: Context, a: Matrix, b: Matrix, tau: float) -> np.ndarray:

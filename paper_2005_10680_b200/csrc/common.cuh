@@ -75,6 +75,8 @@ struct spg_context {
   int device = 0;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // D2H of product chunks overlapping the GEMM
+  cudaStream_t aux_stream = nullptr;   // second compute stream for chunked GEMMs
   cudaEvent_t ev[8] = {};
   std::mutex mu;
   int64_t launches = 0;   // own kernels launched (evidence counter)
@@ -186,7 +188,8 @@ struct CtxGuard {
 // norms.cu
 void leaf_norms(spg_context* ctx, const double* payload, int64_t n_slots, int leaf,
                 int32_t dimension, int32_t nb_logical, const int32_t* slot_rows,
-                const int32_t* slot_cols, double* norms, uint8_t* nonzero, int* bad_padding);
+                const int32_t* slot_cols, double* norms, uint8_t* nonzero, int* bad_padding,
+                cudaStream_t st = nullptr);
 void build_pyramid(spg_context* ctx, spg_matrix* m, const double* slot_norms,
                    const uint8_t* slot_nonzero);
 // matrix.cu
@@ -207,9 +210,19 @@ struct Shard {
 // vectors of the shard (4^level x n_taus, dense (K, J) order) instead of bounds
 void cse_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, const double* taus,
                 int n_taus, double* out, float* ms, Shard shard = {});
-// spamm.cu
+// spamm.cu -- with `host` set, C is streamed to the caller's host buffers
+// chunk by chunk while the GEMM runs and no device matrix is returned
+struct HostOut {
+  int64_t capacity = 0;
+  int32_t* rows = nullptr;
+  int32_t* cols = nullptr;
+  double* payload = nullptr;
+  double* norms = nullptr;
+  int64_t count = 0;
+};
 spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
-                         bool skip_test, spg_spamm_stats* stats, Shard shard = {});
+                         bool skip_test, spg_spamm_stats* stats, Shard shard = {},
+                         HostOut* host = nullptr);
 
 int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
 

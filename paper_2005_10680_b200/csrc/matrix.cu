@@ -337,6 +337,8 @@ int spg_context_create(int device, spg_context** out) {
   SPG_CUDA(cudaSetDevice(device));
   SPG_CUDA(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
   SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  SPG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+  SPG_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
   for (auto& e : ctx->ev) SPG_CUDA(cudaEventCreate(&e));
   *out = ctx.release();
   SPG_API_END
@@ -352,6 +354,8 @@ int spg_context_destroy(spg_context* ctx) {
   ctx->pool.live.clear();
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->stream);
+  cudaStreamDestroy(ctx->copy_stream);
+  cudaStreamDestroy(ctx->aux_stream);
   delete ctx;
   SPG_API_END
 }

@@ -124,17 +124,19 @@ __global__ void pyramid_inner_level(const double* __restrict__ child_level,
 
 void leaf_norms(spg_context* ctx, const double* payload, int64_t n_slots, int leaf,
                 int32_t dimension, int32_t nb_logical, const int32_t* slot_rows,
-                const int32_t* slot_cols, double* norms, uint8_t* nonzero, int* bad_padding) {
+                const int32_t* slot_cols, double* norms, uint8_t* nonzero, int* bad_padding,
+                cudaStream_t st) {
   if (n_slots == 0) return;
+  if (!st) st = ctx->stream;
   const int64_t warps = (n_slots + 31) / 32;
   const unsigned grid = grid_for(warps, kNormWarps);
   const bool check = slot_rows != nullptr && (dimension % leaf) != 0;
   if (check)
-    leaf_norm_kernel<true><<<grid, kNormWarps * 32, 0, ctx->stream>>>(
+    leaf_norm_kernel<true><<<grid, kNormWarps * 32, 0, st>>>(
         payload, n_slots, leaf, dimension, nb_logical, slot_rows, slot_cols, norms, nonzero,
         bad_padding);
   else
-    leaf_norm_kernel<false><<<grid, kNormWarps * 32, 0, ctx->stream>>>(
+    leaf_norm_kernel<false><<<grid, kNormWarps * 32, 0, st>>>(
         payload, n_slots, leaf, dimension, nb_logical, slot_rows, slot_cols, norms, nonzero,
         bad_padding);
   SPG_CHECK_LAUNCH(ctx);

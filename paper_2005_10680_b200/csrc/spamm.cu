@@ -15,6 +15,8 @@
 // >= 1 survivor; its norm follows block_norm (K1); all-zero sums collapse to
 // null (make_leaf); inner norms follow combine_child_norms (K2).
 #include <chrono>
+#include <cstdio>
+#include <cstring>
 #include <cstdlib>
 
 #include <thrust/iterator/counting_iterator.h>
@@ -184,19 +186,19 @@ int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix
 
 template <int L, int KC, int WM, int WN, int NSTAGE>
 void launch_dmma(spg_context* ctx, const double* A, const double* B, const int2* pairs,
-                 const int64_t* out_offset, int64_t n_out, double* C) {
+                 const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st) {
   using Cfg = DmmaGemmCfg<L, KC, WM, WN, NSTAGE>;
   auto kern = leaf_gemm_dmma<L, KC, WM, WN, NSTAGE>;
   SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Cfg::kSmemBytes)));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, ctx->stream>>>(A, B, pairs, out_offset, n_out, C);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(A, B, pairs, out_offset, n_out, C);
   SPG_CHECK_LAUNCH(ctx);
 }
 
 template <int NSTAGE>
 void launch_tma64(spg_context* ctx, const double* A, const double* B, const int2* pairs,
-                  const int64_t* out_offset, int64_t n_out, double* C) {
+                  const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st) {
   using Cfg = TmaGemmCfg<NSTAGE>;
   auto kern = leaf_gemm_tma64<NSTAGE>;
   SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -207,8 +209,8 @@ void launch_tma64(spg_context* ctx, const double* A, const double* B, const int2
   const int64_t grid = std::min<int64_t>(n_out, static_cast<int64_t>(ctx->sm_count) *
                                                     std::max(per_sm, 1));
   DevBuf<unsigned long long> counter(1, ctx);
-  SPG_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), ctx->stream));
-  kern<<<static_cast<unsigned>(grid), Cfg::kThreads, Cfg::kSmemBytes, ctx->stream>>>(
+  SPG_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), st));
+  kern<<<static_cast<unsigned>(grid), Cfg::kThreads, Cfg::kSmemBytes, st>>>(
       A, B, pairs, out_offset, n_out, C, counter.get());
   SPG_CHECK_LAUNCH(ctx);
 }
@@ -222,50 +224,149 @@ int gemm_variant() {
 }
 
 void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const int2* pairs,
-              const int64_t* out_offset, int64_t n_out, double* C) {
+              const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st = nullptr) {
   if (n_out == 0) return;
+  if (!st) st = ctx->stream;
   if (L == 64 && gemm_variant() == 3) {
-    launch_tma64<3>(ctx, A, B, pairs, out_offset, n_out, C);
+    launch_tma64<3>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 4) {  // 4 warps x 32x32, 2 stages, 3 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C);
+    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 5) {  // 4 warps x 32x32, 3 stages, 2 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C);
+    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 6) {  // 4 warps x 32x32, KC=16, 4 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 7) {  // 4 warps x 32x32, KC=16, 6 stages, 2 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C);
+    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   switch (L) {
     case 32:
-      launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C);
+      launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
       break;
     case 64:
-      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C);
+      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
       break;
     case 128:
-      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C);
+      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
       break;
     default: {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
-      leaf_gemm_generic<<<grid, 256, 0, ctx->stream>>>(A, B, pairs, out_offset, n_out, L, C);
+      leaf_gemm_generic<<<grid, 256, 0, st>>>(A, B, pairs, out_offset, n_out, L, C);
       SPG_CHECK_LAUNCH(ctx);
     }
   }
 }
 
+// The product streamed to host buffers: the GEMM runs in chunks of output
+// blocks (Morton order); after each chunk its leaf norms are computed (K1)
+// and the chunk is copied D2H on the copy stream while the next chunk
+// computes.  Result identical to building C on the device and downloading it
+// (same blocks, order, payload and norms; all-zero blocks dropped).
+void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                            DevBuf<int2>& pairs, DevBuf<int64_t>& out_offset,
+                            DevBuf<uint64_t>& out_keys, int64_t n_out, HostOut* host) {
+  const int L = a->leaf;
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  if (n_out > host->capacity) fail(SPG_EINVAL, "output capacity smaller than the product");
+  host->count = 0;
+  if (n_out == 0) return;
+  std::vector<uint64_t> hkeys(static_cast<size_t>(n_out));
+  std::vector<uint8_t> hnz(static_cast<size_t>(n_out));
+  SPG_CUDA(cudaMemcpyAsync(hkeys.data(), out_keys.get(), n_out * sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  DevBuf<double> c_payload(n_out * LL, ctx);
+  DevBuf<double> norms(n_out, ctx);
+  DevBuf<uint8_t> nz(n_out, ctx);
+  const int32_t nb = (a->dimension + L - 1) / L;
+  const int64_t n_chunks = std::min<int64_t>(32, std::max<int64_t>(1, n_out / 4096));
+  const int64_t cs = (n_out + n_chunks - 1) / n_chunks;
+  std::vector<cudaEvent_t> done(static_cast<size_t>(n_chunks));
+  for (auto& e : done) SPG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct EventGuard {
+    std::vector<cudaEvent_t>& v;
+    ~EventGuard() {
+      for (auto& e : v) cudaEventDestroy(e);
+    }
+  } guard{done};
+  {
+    PhaseTrace tr(ctx, "gemm+stream");
+    // chunks alternate between two compute streams so one chunk's tail
+    // (uneven survivor counts per block) overlaps the next chunk's head
+    cudaStream_t cs_[2] = {ctx->stream, ctx->aux_stream};
+    cudaEvent_t ready;
+    SPG_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    SPG_CUDA(cudaEventRecord(ready, ctx->stream));
+    SPG_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ready, 0));
+    cudaEventDestroy(ready);
+    static const int dbg = [] {
+      const char* e = std::getenv("SPG_STREAM_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    const auto tq0 = std::chrono::steady_clock::now();
+    for (int64_t c = 0; c < n_chunks; ++c) {
+      const int64_t o0 = c * cs, o1 = std::min(n_out, o0 + cs);
+      if (o0 >= o1) break;
+      cudaStream_t st = cs_[c & 1];
+      if (dbg == 2) {  // no copies at all
+        run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get() + o0, o1 - o0,
+                 c_payload.get() + o0 * LL, st);
+        continue;
+      }
+      run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get() + o0, o1 - o0,
+               c_payload.get() + o0 * LL, st);
+      leaf_norms(ctx, c_payload.get() + o0 * LL, o1 - o0, L, a->dimension, nb, nullptr, nullptr,
+                 norms.get() + o0, nz.get() + o0, nullptr, st);
+      SPG_CUDA(cudaEventRecord(done[c], st));
+      SPG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, done[c], 0));
+      SPG_CUDA(cudaMemcpyAsync(host->payload + o0 * LL, c_payload.get() + o0 * LL,
+                               (o1 - o0) * LL * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->copy_stream));
+      SPG_CUDA(cudaMemcpyAsync(host->norms + o0, norms.get() + o0, (o1 - o0) * sizeof(double),
+                               cudaMemcpyDeviceToHost, ctx->copy_stream));
+    }
+    // the all-zero flags go to pageable host memory: one copy after the loop
+    // (a pageable cudaMemcpyAsync blocks the host and would serialise the chunks)
+    if (dbg)
+      std::fprintf(stderr, "[spg] enqueue loop %.3f ms\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tq0).count());
+    // join: the pool's stream order requires the main stream to see all work
+    SPG_CUDA(cudaEventRecord(done[0], ctx->copy_stream));
+    SPG_CUDA(cudaStreamWaitEvent(ctx->stream, done[0], 0));
+    SPG_CUDA(cudaEventRecord(done[0], ctx->aux_stream));
+    SPG_CUDA(cudaStreamWaitEvent(ctx->stream, done[0], 0));
+    SPG_CUDA(cudaMemcpyAsync(hnz.data(), nz.get(), n_out, cudaMemcpyDeviceToHost, ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->aux_stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  // keys -> coordinates; drop the (rare) all-zero sums like make_leaf
+  int64_t kept = 0;
+  for (int64_t o = 0; o < n_out; ++o) {
+    if (!hnz[o]) continue;
+    if (kept != o) {
+      std::memmove(host->payload + kept * LL, host->payload + o * LL, LL * sizeof(double));
+      host->norms[kept] = host->norms[o];
+    }
+    const uint64_t key = hkeys[o];
+    if (host->rows) host->rows[kept] = static_cast<int32_t>(morton_row(key));
+    if (host->cols) host->cols[kept] = static_cast<int32_t>(morton_col(key));
+    ++kept;
+  }
+  host->count = kept;
+}
+
 }  // namespace
 
 spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
-                         bool skip_test, spg_spamm_stats* stats, Shard shard) {
+                         bool skip_test, spg_spamm_stats* stats, Shard shard, HostOut* host) {
   if (a->dimension != b->dimension || a->leaf != b->leaf)
     fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
   if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
@@ -313,21 +414,28 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   }
   tl.keys.reset();
   SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
-  double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
-  {
-  PhaseTrace tr(ctx, "gemm");
-  run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload);
-  }
-  SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
-  pairs.reset();
-  out_offset.reset();
   spg_matrix* c = nullptr;
-  {
-    PhaseTrace tr(ctx, "finalize");
-    c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, out_keys.release(), c_payload);
+  if (host) {
+    stream_product_to_host(ctx, a, b, pairs, out_offset, out_keys, n_out, host);
+    SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+    SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+    SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
+  } else {
+    double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+    {
+      PhaseTrace tr(ctx, "gemm");
+      run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload);
+    }
+    SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+    pairs.reset();
+    out_offset.reset();
+    {
+      PhaseTrace tr(ctx, "finalize");
+      c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, out_keys.release(), c_payload);
+    }
+    SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+    SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   }
-  SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
-  SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   if (stats) {
     stats->survivors = n_surv;
     stats->output_blocks = n_out;
@@ -420,6 +528,53 @@ int spg_spamm_shard(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, 
   *c = nullptr;
   CtxGuard g(ctx);
   *c = spamm_device(ctx, a, b, tau, true, stats, Shard{level, shard});
+  SPG_API_END
+}
+
+int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
+                                         const spg_matrix* b, double delta, const double* taus,
+                                         int32_t n_taus, int64_t capacity, int32_t* c_rows,
+                                         int32_t* c_cols, double* c_payload, double* c_norms,
+                                         int64_t* c_count, double* bounds,
+                                         spg_controlled_stats* stats) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !c_payload || !c_norms || !c_count) fail(SPG_EINVAL, "null argument");
+  if (!(delta > 0.0)) fail(SPG_EINVAL, "spamm_with_error_control: delta must be positive");
+  int rc = spg_tolerance_grid_check(taus, n_taus);
+  if (rc != SPG_OK) return rc;
+  CtxGuard g(ctx);
+  std::vector<double> local(static_cast<size_t>(n_taus));
+  double* bv = bounds ? bounds : local.data();
+  float cse_ms = 0.0f;
+  const auto t0 = Clock::now();
+  cse_device(ctx, a, b, taus, n_taus, bv, &cse_ms);
+  const double cse_seconds = seconds_since(t0);
+  int32_t k = -1;
+  for (int32_t i = 0; i < n_taus; ++i)
+    if (bv[i] < delta) {
+      k = i;
+      break;
+    }
+  const double tau = k >= 0 ? taus[k] : 0.0;
+  HostOut out;
+  out.capacity = capacity;
+  out.rows = c_rows;
+  out.cols = c_cols;
+  out.payload = c_payload;
+  out.norms = c_norms;
+  spg_spamm_stats ss{};
+  const auto t1 = Clock::now();
+  spamm_device(ctx, a, b, tau, true, stats ? &ss : nullptr, Shard{}, &out);
+  *c_count = out.count;
+  if (stats) {
+    stats->tau = tau;
+    stats->tau_index = k;
+    stats->bound = k >= 0 ? bv[k] : 0.0;
+    stats->cse_seconds = cse_seconds;
+    stats->spamm_seconds = seconds_since(t1);
+    stats->ms_cse = cse_ms;
+    stats->spamm = ss;
+  }
   SPG_API_END
 }
 

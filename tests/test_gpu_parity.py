@@ -149,3 +149,25 @@ def test_run_to_run_determinism(ctx):
     for b, (r, c, p, nrm) in outs[1:]:
         assert bits_equal(b, outs[0][0])
         assert bits_equal(p, outs[0][1][2]) and bits_equal(nrm, outs[0][1][3])
+
+
+@pytest.mark.parametrize("L", [16, 64])
+def test_streamed_to_host_equals_device_product(ctx, L):
+    """spg_spamm_with_error_control_to_host (chunked GEMM + overlapped D2H) ==
+    spg_spamm_with_error_control + spg_matrix_download, bit for bit."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    n = 64 * L
+    rows, cols, pay = nat.synth_chain_host(n, L, 40.0, 7, 1e-10)
+    A = nat.upload(ctx, n, L, rows, cols, pay)
+    taus = log_grid(32)
+    C, st, b = nat.spamm_with_error_control(ctx, A, A, 1e-6, taus)
+    r, c, p, nrm = C.download()
+    (hr, hc, hp, hn), hst, hb = nat.spamm_with_error_control_to_host(ctx, A, A, 1e-6, taus)
+    assert bits_equal(b, hb) and hst["tau"] == st["tau"]
+    assert np.array_equal(r, hr) and np.array_equal(c, hc)
+    assert bits_equal(p, hp) and bits_equal(nrm, hn)
+    with pytest.raises(ValueError):
+        nat.spamm_with_error_control_to_host(
+            ctx, A, A, 1e-6, taus, out=(np.empty(1, np.int32), np.empty(1, np.int32),
+                                        np.empty((1, L * L)), np.empty(1)))
