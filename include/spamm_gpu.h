@@ -157,6 +157,32 @@ int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
 int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                   int64_t* count, int32_t* triples, int64_t capacity);
 
+/* ---- callers of the hot path (SURVEY.md 8f "next" row 1) ----------------- */
+/* truncate (error_control.hpp:59-62, error_control.cpp:174-201): remove whole
+ * leaves greedily in ascending (norm, row-major position) order while the
+ * removed norm stays strictly below delta.  The result shares x's payload. */
+int spg_truncate(spg_context* ctx, const spg_matrix* x, double delta, spg_matrix** out,
+                 double* removed_norm_bound, int64_t* removed_block_count);
+
+#define SPG_VARIANT_TRUNCMUL 0 /* multiply_exact + truncate(delta)              */
+#define SPG_VARIANT_SPAMM 1    /* spamm_with_error_control(delta)                */
+#define SPG_VARIANT_HYBRID 2   /* spamm_with_error_control(delta/2) + truncate(delta/2) */
+
+typedef struct {
+  int32_t variant;
+  double chosen_tau;         /* RunRecord::chosen_tau (0 for truncmul)        */
+  int64_t nnz_blocks_mid;    /* leaves of the product before truncation       */
+  int64_t removed_blocks;    /* leaves removed by truncation                  */
+  double removed_norm_bound; /* sqrt of the removed squared norms             */
+  double t_mul, t_cse, t_spamm, t_trunc; /* host seconds per phase (RunRecord) */
+  double flops;              /* leaf-GEMM flops performed                     */
+} spg_square_stats;
+
+/* approximate_square (experiment.cpp:47-82): X*X by one of the variants. */
+int spg_approximate_square(spg_context* ctx, const spg_matrix* x, int32_t variant, double delta,
+                           const double* taus, int32_t n_taus, spg_matrix** out,
+                           spg_square_stats* stats);
+
 /* ---- row shards across GPUs (new, the reference is single-
  * process) --------------------------------------------------------------
  * A shard at `level` s owns output block-rows [shard*nb/2^s, (shard+1)*nb/2^s)

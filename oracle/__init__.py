@@ -114,6 +114,8 @@ class Oracle:
         self._spamm = fn("spamm", _vp, [_vp, _vp, C.c_double, C.POINTER(C.c_int)])
         self._exact = fn("multiply_exact", _vp, [_vp, _vp, C.POINTER(C.c_int)])
         self._surv = fn("survivors", C.c_int64, [_vp, _vp, C.c_double, _i32p, C.c_int64])
+        self._trunc = fn("truncate", _vp, [_vp, C.c_double, _dp, C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int)])
         self._cse_sub = fn("cse_subtree", C.c_int, [_vp, _vp, _dp, C.c_int, C.c_int, C.c_int32,
                                                    C.c_int32, C.c_int32, _dp])
         if kind == "port":
@@ -193,6 +195,16 @@ class Oracle:
         if st.value != 0 or not h:
             raise ValueError("multiply: invalid arguments")
         return Tree(self, h, a.leaf)
+
+    def truncate(self, x: Tree, delta: float):
+        """(tree, removed_norm_bound, removed_block_count)."""
+        rn = C.c_double(0)
+        rc = C.c_int64(0)
+        st = C.c_int(0)
+        h = self._trunc(x.h, delta, C.byref(rn), C.byref(rc), C.byref(st))
+        if st.value != 0 or not h:
+            raise ValueError("truncate: delta must be nonnegative")
+        return Tree(self, h, x.leaf), rn.value, rc.value
 
     def survivors(self, a: Tree, b: Tree, tau: float) -> np.ndarray:
         n = self._surv(a.h, b.h, tau, None, 0)

@@ -310,6 +310,25 @@ void* ref_spamm_with_error_control(const void* a, const void* b, double delta, c
   }
 }
 
+// spamm::truncate (error_control.cpp:174-201)
+void* ref_truncate(const void* x, double delta, double* removed_norm, std::int64_t* removed_count,
+                   int* status) {
+  try {
+    const auto* r = static_cast<const RefTree*>(x);
+    auto res = spamm::truncate(r->m, delta);
+    auto* out = new RefTree;
+    out->m = std::move(res.matrix);
+    out->depth = r->depth;
+    if (removed_norm) *removed_norm = res.removed_norm_bound;
+    if (removed_count) *removed_count = res.removed_block_count;
+    if (status) *status = 0;
+    return out;
+  } catch (const std::exception&) {
+    if (status) *status = -1;
+    return nullptr;
+  }
+}
+
 std::int64_t ref_survivors(const void* a, const void* b, double tau, std::int32_t* triples,
                            std::int64_t capacity) {
   const auto* ra = static_cast<const RefTree*>(a);

@@ -518,3 +518,72 @@ int64_t ora_candidates(const ora_tree* a, const ora_tree* b) {
   surv_node(&s, a->root, b->root, 0, 0, 0, 0);
   return s.count;
 }
+
+/* ---------------------------------------------------------------------------
+ * Truncation: error_control.cpp:93-134 (collect_leaves / drop_leaves),
+ * :174-201 (truncate)
+ * ------------------------------------------------------------------------- */
+
+typedef struct {
+  double norm;
+  int64_t position; /* block_row * blocks_per_side + block_col */
+  int64_t index;    /* Morton-order leaf index */
+} leaf_ref;
+
+static int cmp_leaf_ref(const void* x, const void* y) {
+  const leaf_ref* a = (const leaf_ref*)x;
+  const leaf_ref* b = (const leaf_ref*)y;
+  if (a->norm != b->norm) return a->norm < b->norm ? -1 : 1;
+  return (a->position > b->position) - (a->position < b->position);
+}
+
+ora_tree* ora_truncate(const ora_tree* x, double delta, double* removed_norm,
+                       int64_t* removed_count, int* status) {
+  if (delta < 0.0) {
+    if (status) *status = -1;
+    return NULL;
+  }
+  const int64_t n = ora_nnz_blocks(x);
+  const int64_t L2 = (int64_t)x->leaf_size * x->leaf_size;
+  const int64_t side = (int64_t)1 << x->depth;
+  int32_t* rows = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  int32_t* cols = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  double* norms = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  double* payload = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n * L2 : 1));
+  ora_leaves(x, rows, cols, payload, norms);
+  leaf_ref* refs = (leaf_ref*)malloc(sizeof(leaf_ref) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) {
+    refs[i].norm = norms[i];
+    refs[i].position = (int64_t)rows[i] * side + cols[i];
+    refs[i].index = i;
+  }
+  qsort(refs, (size_t)n, sizeof(leaf_ref), cmp_leaf_ref);
+  char* removed = (char*)calloc((size_t)(n > 0 ? n : 1), 1);
+  double sumsq = 0.0;
+  int64_t count = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(sqrt(sumsq + refs[i].norm * refs[i].norm) < delta)) break;
+    sumsq += refs[i].norm * refs[i].norm;
+    removed[refs[i].index] = 1;
+    ++count;
+  }
+  int64_t kept = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (removed[i]) continue;
+    rows[kept] = rows[i];
+    cols[kept] = cols[i];
+    memmove(payload + kept * L2, payload + i * L2, sizeof(double) * (size_t)L2);
+    ++kept;
+  }
+  ora_tree* out = ora_build(x->dimension, x->leaf_size, kept, rows, cols, payload);
+  free(rows);
+  free(cols);
+  free(norms);
+  free(payload);
+  free(refs);
+  free(removed);
+  if (removed_norm) *removed_norm = sqrt(sumsq);
+  if (removed_count) *removed_count = count;
+  if (status) *status = 0;
+  return out;
+}

@@ -85,6 +85,12 @@ int64_t ora_survivors(const ora_tree* a, const ora_tree* b, double tau, int32_t*
 /* Number of non-null leaf pairs (candidates T_cand, SURVEY 8 notation). */
 int64_t ora_candidates(const ora_tree* a, const ora_tree* b);
 
+/* truncate (error_control.cpp:93-134,174-201): returns the truncated tree
+ * (a new tree; leaves copied), the removed norm bound and count; NULL with
+ * *status = -1 for delta < 0. */
+ora_tree* ora_truncate(const ora_tree* x, double delta, double* removed_norm,
+                       int64_t* removed_count, int* status);
+
 /* Leaf norm rule alone (node_ops.hpp:24-28), for kernel-level pins. */
 double ora_block_norm(const double* block, int64_t count);
 

@@ -55,6 +55,19 @@ class SpammStats(C.Structure):
         return {f: getattr(self, f) for f, _ in self._fields_}
 
 
+class SquareStats(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("chosen_tau", C.c_double), ("nnz_blocks_mid", C.c_int64),
+                ("removed_blocks", C.c_int64), ("removed_norm_bound", C.c_double),
+                ("t_mul", C.c_double), ("t_cse", C.c_double), ("t_spamm", C.c_double),
+                ("t_trunc", C.c_double), ("flops", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+VARIANTS = {"truncmul": 0, "spamm": 1, "hybrid": 2}
+
+
 class ControlledStats(C.Structure):
     _fields_ = [("tau", C.c_double), ("tau_index", C.c_int32), ("bound", C.c_double),
                 ("cse_seconds", C.c_double), ("spamm_seconds", C.c_double),
@@ -97,6 +110,9 @@ _SIGNATURES = {
     "spg_spamm_with_error_control_to_host": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
                                                        C.c_int64, _i32p, _i32p, _dp, _dp, _i64p,
                                                        _dp, C.POINTER(ControlledStats)]),
+    "spg_truncate": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(_vp), _dp, _i64p]),
+    "spg_approximate_square": (C.c_int, [_vp, _vp, C.c_int32, C.c_double, _dp, C.c_int32,
+                                         C.POINTER(_vp), C.POINTER(SquareStats)]),
     "spg_cse_shard": (C.c_int, [_vp, _vp, _vp, _dp, C.c_int32, C.c_int32, C.c_int32, _dp]),
     "spg_cse_finish": (C.c_int, [C.c_int32, _dp, _dp, C.c_int32, _dp, _dp]),
     "spg_matrix_top_norms": (C.c_int, [_vp, C.c_int32, _dp]),
@@ -389,6 +405,27 @@ def survivors(ctx: Context, a: Matrix, b: Matrix, tau: float) -> np.ndarray:
         _check(lib().spg_survivors(ctx.handle, a.handle, b.handle, tau, C.byref(count),
                                    _ptr(out, C.c_int32), count.value))
     return out
+
+
+# ---------------------------------------------------------------- callers
+def truncate(ctx: Context, x: Matrix, delta: float):
+    """(matrix, removed_norm_bound, removed_block_count) -- error_control.cpp:174-201."""
+    h = _vp()
+    rn = C.c_double(0)
+    rc = C.c_int64(0)
+    _check(lib().spg_truncate(ctx.handle, x.handle, delta, C.byref(h), C.byref(rn), C.byref(rc)))
+    return Matrix(ctx, h), rn.value, rc.value
+
+
+def approximate_square(ctx: Context, x: Matrix, variant: str, delta: float, taus):
+    """experiment.cpp:47-82 approximate_square; variant truncmul | spamm | hybrid."""
+    taus = np.ascontiguousarray(taus, np.float64)
+    h = _vp()
+    st = SquareStats()
+    _check(lib().spg_approximate_square(ctx.handle, x.handle, VARIANTS[variant], delta,
+                                        _ptr(taus, C.c_double), taus.size, C.byref(h),
+                                        C.byref(st)))
+    return Matrix(ctx, h), st.as_dict()
 
 
 # ---------------------------------------------------------------- row shards (SURVEY 8e)

@@ -18,6 +18,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <stdexcept>
@@ -89,7 +90,8 @@ struct spg_matrix {
   int32_t dimension = 0, padded = 0, leaf = 0, depth = 0;
   int64_t nnzb = 0;     // non-null leaves
   int64_t n_slots = 0;  // payload slots (>= nnzb)
-  double* payload = nullptr;    // n_slots * L * L
+  double* payload = nullptr;    // n_slots * L * L (owned through payload_ref)
+  std::shared_ptr<double> payload_ref;  // shared by matrices derived without copying (truncate)
   uint64_t* keys = nullptr;     // nnzb Morton keys, ascending
   int32_t* slots = nullptr;     // nnzb payload slots, aligned with keys
   int32_t* grid_slot = nullptr; // 4^depth
@@ -200,6 +202,13 @@ spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32
                                       int64_t n_blocks, uint64_t* d_keys_owned,
                                       double* d_payload_owned);
 void matrix_destroy(spg_matrix* m);
+// New matrix over x's payload (shared) keeping the slots with keep[slot] != 0;
+// slot_norms[slot] = cached leaf norm (K1 result) for kept slots.
+spg_matrix* matrix_keep_slots(spg_context* ctx, const spg_matrix* x, const double* slot_norms,
+                              const uint8_t* keep);
+// truncate.cu
+spg_matrix* truncate_device(spg_context* ctx, const spg_matrix* x, double delta,
+                            double* removed_norm, int64_t* removed_count);
 void check_shape(int32_t dimension, int32_t leaf, int32_t* padded, int32_t* depth);
 // Row shard of a product: level 0 = the whole matrix.
 struct Shard {

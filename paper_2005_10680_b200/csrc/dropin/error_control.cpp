@@ -1,6 +1,5 @@
-// error_control.cpp -- drop-in CSE sweep, selection and controlled product
-// (error_control.hpp:18-77) on the GPU path; truncate() is a host operation
-// outside the hot path (SURVEY.md 8f "next").
+// error_control.cpp -- drop-in CSE sweep, selection, truncation and
+// controlled product (error_control.hpp:18-77), all on the GPU path.
 #include "spamm/error_control.hpp"
 
 #include <algorithm>
@@ -54,47 +53,18 @@ SpammTolerance select_tolerance(const ErrorBoundVector& bounds, const ToleranceG
 }
 
 TruncationResult truncate(const QuadTreeMatrix& x, double delta) {
-  // Greedy removal in ascending (norm, row-major position) order while the
-  // removed norm stays strictly below delta (error_control.hpp:59-62).
+  // GPU greedy truncation (spg_truncate): same removed set, bound and norms as
+  // error_control.cpp:174-201; the result shares x's leaf payload.
   if (delta < 0.0) throw std::invalid_argument("truncate: delta must be nonnegative");
-  spg_matrix_info info{};
-  b200::check(spg_matrix_get_info(x.device(), &info));
-  const int L = x.leaf_size();
-  const size_t n = static_cast<size_t>(info.nnz_blocks);
-  std::vector<int32_t> rows(n), cols(n);
-  std::vector<double> norms(n), payload(n * static_cast<size_t>(L) * L);
-  if (n) b200::check(spg_matrix_download(x.device(), rows.data(), cols.data(), payload.data(), norms.data()));
-  const int64_t side = x.padded_dimension() / L;
-  std::vector<size_t> order(n);
-  for (size_t i = 0; i < n; ++i) order[i] = i;
-  std::sort(order.begin(), order.end(), [&](size_t p, size_t q) {
-    const int64_t pp = rows[p] * side + cols[p], pq = rows[q] * side + cols[q];
-    return norms[p] != norms[q] ? norms[p] < norms[q] : pp < pq;
-  });
-  std::vector<char> removed(n, 0);
-  double sumsq = 0.0;
+  spg_matrix* m = nullptr;
+  double removed = 0.0;
   int64_t count = 0;
-  for (size_t i : order) {
-    if (!(std::sqrt(sumsq + norms[i] * norms[i]) < delta)) break;
-    sumsq += norms[i] * norms[i];
-    removed[i] = 1;
-    ++count;
-  }
-  TruncationResult result{x, std::sqrt(sumsq), count};
+  b200::check(spg_truncate(b200::context(), x.device(), delta, &m, &removed, &count));
+  TruncationResult result{x, removed, count};
   if (count > 0) {
-    std::vector<int32_t> kr, kc;
-    std::vector<double> kp;
-    const size_t LL = static_cast<size_t>(L) * L;
-    for (size_t i = 0; i < n; ++i)
-      if (!removed[i]) {
-        kr.push_back(rows[i]);
-        kc.push_back(cols[i]);
-        kp.insert(kp.end(), payload.begin() + i * LL, payload.begin() + (i + 1) * LL);
-      }
-    spg_matrix* m = nullptr;
-    b200::check(spg_matrix_upload(b200::context(), x.dimension(), L, static_cast<int64_t>(kr.size()),
-                                  kr.data(), kc.data(), kp.data(), &m));
     result.matrix = adopt_device(m);
+  } else {
+    spg_matrix_free(m);  // nothing removed: share x itself (root() identity, :197-198)
   }
   return result;
 }

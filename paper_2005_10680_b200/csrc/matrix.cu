@@ -246,7 +246,7 @@ __global__ void gather_norms(const uint64_t* __restrict__ keys, int64_t n,
 void matrix_destroy(spg_matrix* m) {
   if (!m) return;
   spg_context* ctx = m->ctx;
-  dev_free(m->payload, ctx);
+  m->payload_ref.reset();  // returns the payload to the pool with its last user
   dev_free(m->keys, ctx);
   dev_free(m->slots, ctx);
   dev_free(m->grid_slot, ctx);
@@ -265,6 +265,8 @@ spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32
     throw;
   }
   m->payload = d_payload_owned;
+  m->payload_ref = std::shared_ptr<double>(d_payload_owned,
+                                           [ctx](double* p) { dev_free(p, ctx); });
   m->n_slots = n_leaves;
   if (n_leaves > (int64_t(1) << 31) - 1) fail(SPG_EINVAL, "too many leaves");
   const int32_t nb_logical = (dimension + leaf - 1) / leaf;
@@ -285,6 +287,26 @@ spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32
   return m.release();
 }
 
+spg_matrix* matrix_keep_slots(spg_context* ctx, const spg_matrix* x, const double* slot_norms,
+                              const uint8_t* keep) {
+  std::unique_ptr<spg_matrix, void (*)(spg_matrix*)> m(new_matrix(ctx, x->dimension, x->leaf),
+                                                       matrix_destroy);
+  m->payload = x->payload;
+  m->payload_ref = x->payload_ref;
+  m->n_slots = x->n_slots;
+  const int64_t cells = int64_t(1) << (2 * x->depth);
+  SPG_CUDA(cudaMemcpyAsync(m->grid_slot, x->grid_slot, cells * sizeof(int32_t),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+  build_pyramid(ctx, m.get(), slot_norms, keep);  // removed slots -> null
+  compact_leaves(ctx, m.get());
+  double root = -1.0;
+  SPG_CUDA(cudaMemcpyAsync(&root, m->pyramid, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  m->frob = root < 0.0 ? 0.0 : root;
+  return m.release();
+}
+
 spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32_t leaf,
                                       int64_t n_blocks, uint64_t* d_keys_owned,
                                       double* d_payload_owned) {
@@ -297,6 +319,8 @@ spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32
     throw;
   }
   m->payload = d_payload_owned;
+  m->payload_ref = std::shared_ptr<double>(d_payload_owned,
+                                           [ctx](double* p) { dev_free(p, ctx); });
   m->n_slots = n_blocks;
   DevBuf<uint64_t> keys = DevBuf<uint64_t>::adopt(d_keys_owned, n_blocks, ctx);
   DevBuf<int32_t> rows(std::max<int64_t>(n_blocks, 1), ctx);

@@ -59,6 +59,15 @@ def record_case(R, name, n, L, la, lb, taus, taus_list, deltas):
     for i, d in enumerate(deltas):
         out[f"delta{i}"] = np.float64(d)
         out[f"select{i}"] = np.int64(R.select_index(out["bounds"], d))
+    # truncation of A (error_control.cpp:174-201) at fractions of ||A||_F
+    for i, f in enumerate((0.0, 0.05, 0.3, 1.01)):
+        d = f * ta.frobenius()
+        tt, rn, rc = R.truncate(ta, d)
+        r, c, _, nrm = tt.leaves(payload=False)
+        out[f"trunc{i}_delta"] = np.float64(d)
+        out[f"trunc{i}_removed_norm"] = np.float64(rn)
+        out[f"trunc{i}_removed_count"] = np.int64(rc)
+        out[f"trunc{i}_rows"], out[f"trunc{i}_cols"], out[f"trunc{i}_norms"] = r, c, nrm
     np.savez_compressed(OUT / f"{name}.npz", **out)
     return out
 

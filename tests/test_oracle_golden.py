@@ -103,3 +103,19 @@ def test_norm_only_tree_matches_full_tree(port):
     rb, cb, _, nb = tb.leaves(payload=False)
     tbn = port.build_norm_only(int(g["n"]), int(g["L"]), rb, cb, nb)
     assert bits_equal(port.cse(tn, tbn, g["taus"]), g["bounds"])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_port_truncate_matches_reference_golden(port, name):
+    g = load_golden(name)
+    ta = _build(port, g, "a")
+    i = 0
+    while f"trunc{i}_delta" in g:
+        t, rn, rc = port.truncate(ta, float(g[f"trunc{i}_delta"]))
+        assert rc == int(g[f"trunc{i}_removed_count"])
+        assert bits_equal(rn, g[f"trunc{i}_removed_norm"])
+        r, c, _, nrm = t.leaves(payload=False)
+        assert np.array_equal(r, g[f"trunc{i}_rows"]) and np.array_equal(c, g[f"trunc{i}_cols"])
+        assert bits_equal(nrm, g[f"trunc{i}_norms"])
+        i += 1
+    assert i == 4
