@@ -183,6 +183,59 @@ int spg_approximate_square(spg_context* ctx, const spg_matrix* x, int32_t varian
                            const double* taus, int32_t n_taus, spg_matrix** out,
                            spg_square_stats* stats);
 
+/* ---- device matrix algebra for the callers (quadtree.cpp:128-171,254-261) */
+/* QuadTreeMatrix::trace: same association as node_trace (quadtree.cpp:128-138). */
+int spg_matrix_trace(const spg_matrix* m, double* out);
+/* QuadTreeMatrix::nnz: stored entries != 0 (quadtree.cpp:140-151). */
+int spg_matrix_nnz(const spg_matrix* m, int64_t* out);
+/* add(a.scale(alpha), b.scale(beta)) (quadtree.cpp:24-36,249-261); b may be
+ * NULL (scale only).  All-zero leaves collapse. */
+int spg_matrix_axpby(spg_context* ctx, double alpha, const spg_matrix* a, double beta,
+                     const spg_matrix* b, spg_matrix** out);
+/* QuadTreeMatrix::identity (quadtree.cpp:231-235). */
+int spg_matrix_identity(spg_context* ctx, int32_t dimension, int32_t leaf_size, spg_matrix** out);
+
+/* ---- SP2 purification over the GPU product (purification.cpp:49-202;
+ * SURVEY.md 8f row 2, BASELINE config 3) ----------------------------------- */
+#define SPG_STATUS_OK 0
+#define SPG_STATUS_VIOLATION 1
+#define SPG_STATUS_CONVERGED 2
+
+typedef struct {
+  int32_t variant;               /* SPG_VARIANT_*                               */
+  int32_t occupation;            /* PurificationConfig::occupation             */
+  int32_t max_iterations;
+  double epsilon;
+  double idempotency_threshold;  /* 0 -> epsilon / 10                          */
+  const double* taus;            /* tolerance grid of the controlled products  */
+  int32_t n_taus;
+  double initial_delta;          /* ErrorBudget::initial_delta                 */
+  const double* deltas;          /* ErrorBudget::deltas (>= max_iterations)    */
+  int32_t n_deltas;
+  int32_t measure_error;         /* realized error vs an exact product (RunRecord) */
+} spg_purify_config;
+
+/* RunRecord (run_record.hpp:16-32), one per iteration (0 = initial truncation) */
+typedef struct {
+  int32_t iteration;
+  int32_t status;      /* SPG_STATUS_*                          */
+  int32_t polynomial;  /* 0: x^2, 1: 2x - x^2 (sp2_step)         */
+  double tolerance, chosen_tau, t_mul, t_trunc, t_spamm, t_cse;
+  int64_t nnz_in, nnz_mid, nnz_out, nnz_blocks_out;
+  double realized_error; /* -1 when not measured                 */
+  double trace;
+  double flops;          /* leaf-GEMM flops of the iteration's square */
+} spg_run_record;
+
+/* ErrorBudget::geometric (purification.cpp:66-82): deltas[iterations]. */
+int spg_error_budget_geometric(double epsilon, int32_t iterations, double ratio,
+                               double* initial_delta, double* deltas);
+/* purify (purification.cpp:90-202).  *density: the final iterate (or the last
+ * iterate before convergence, like the reference). */
+int spg_purify(spg_context* ctx, const spg_matrix* x0, const spg_purify_config* cfg,
+               spg_matrix** density, spg_run_record* log, int32_t log_capacity, int32_t* n_log,
+               int32_t* converged, int32_t* iterations);
+
 /* ---- row shards across GPUs (new, the reference is single-
  * process) --------------------------------------------------------------
  * A shard at `level` s owns output block-rows [shard*nb/2^s, (shard+1)*nb/2^s)

@@ -124,6 +124,10 @@ class Oracle:
         else:
             self._from_dense = fn("from_dense", _vp, [C.c_int, C.c_int, _dp])
             self._threads = fn("set_max_threads", None, [C.c_int])
+            self._purify = fn("purify", _vp, [_vp, C.c_int, C.c_int, C.c_int, C.c_double, _dp,
+                                              C.c_int, C.c_double, _dp, C.c_double, C.c_int,
+                                              C.POINTER(C.c_int), _dp, C.POINTER(C.c_int),
+                                              C.POINTER(C.c_int)])
             self._swec = fn("spamm_with_error_control", _vp,
                             [_vp, _vp, C.c_double, _dp, C.c_int, _dp, _dp, _dp, _dp,
                              C.POINTER(C.c_int)])
@@ -205,6 +209,23 @@ class Oracle:
         if st.value != 0 or not h:
             raise ValueError("truncate: delta must be nonnegative")
         return Tree(self, h, x.leaf), rn.value, rc.value
+
+    def purify(self, x0: Tree, variant: int, occupation: int, max_iterations: int, epsilon: float,
+               taus, initial_delta: float, deltas, idempotency_threshold: float = 0.0):
+        """Reference purify (ref back end only): (tree, log rows, converged, iterations);
+        log rows = (iteration, status, chosen_tau, trace, realized_error, nnz_out)."""
+        taus = np.ascontiguousarray(taus, np.float64)
+        deltas = np.ascontiguousarray(deltas, np.float64)
+        cap = max_iterations + 2
+        log = np.zeros((cap, 6))
+        n_log, conv, its = C.c_int(0), C.c_int(0), C.c_int(0)
+        h = self._purify(x0.h, variant, occupation, max_iterations, epsilon,
+                         _p(taus, C.c_double), taus.size, initial_delta, _p(deltas, C.c_double),
+                         idempotency_threshold, cap, C.byref(n_log), _p(log, C.c_double),
+                         C.byref(conv), C.byref(its))
+        if not h:
+            raise ValueError("purify: invalid configuration")
+        return Tree(self, h, x0.leaf), log[:min(n_log.value, cap)], bool(conv.value), its.value
 
     def survivors(self, a: Tree, b: Tree, tau: float) -> np.ndarray:
         n = self._surv(a.h, b.h, tau, None, 0)

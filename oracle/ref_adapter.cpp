@@ -19,6 +19,7 @@
 #include "spamm/error_control.hpp"
 #include "spamm/execution.hpp"
 #include "spamm/multiply.hpp"
+#include "spamm/purification.hpp"
 #include "spamm/quadtree.hpp"
 
 namespace {
@@ -325,6 +326,55 @@ void* ref_truncate(const void* x, double delta, double* removed_norm, std::int64
     return out;
   } catch (const std::exception&) {
     if (status) *status = -1;
+    return nullptr;
+  }
+}
+
+// spamm::purify (purification.cpp:90-202) with an explicit budget.  Writes
+// per-record (iteration, status 0 ok/1 violation/2 converged, chosen_tau,
+// trace, realized_error, nnz_out) and returns the density tree.
+void* ref_purify(const void* x0, int variant, int occupation, int max_iterations, double epsilon,
+                 const double* taus, int n_taus, double initial_delta, const double* deltas,
+                 double idempotency_threshold, int log_capacity, int* n_log, double* log6,
+                 int* converged, int* iterations) {
+  try {
+    spamm::PurificationConfig cfg;
+    cfg.variant = static_cast<spamm::Variant>(variant);
+    cfg.occupation = occupation;
+    cfg.max_iterations = max_iterations;
+    cfg.epsilon = epsilon;
+    cfg.grid = spamm::ToleranceGrid(std::vector<double>(taus, taus + n_taus));
+    cfg.idempotency_threshold = idempotency_threshold;
+    std::vector<double> dv(deltas, deltas + max_iterations);
+    cfg.budget = [initial_delta, dv](double, int) {
+      spamm::ErrorBudget b;
+      b.initial_delta = initial_delta;
+      b.deltas = dv;
+      return b;
+    };
+    const auto* r = static_cast<const RefTree*>(x0);
+    auto res = spamm::purify(r->m, cfg);
+    int k = 0;
+    for (const auto& rec : res.log) {
+      if (k < log_capacity) {
+        double* o = log6 + 6 * k;
+        o[0] = rec.iteration;
+        o[1] = rec.status == "ok" ? 0 : rec.status == "violation" ? 1 : 2;
+        o[2] = rec.chosen_tau;
+        o[3] = rec.trace;
+        o[4] = rec.realized_error;
+        o[5] = static_cast<double>(rec.nnz_out);
+      }
+      ++k;
+    }
+    *n_log = k;
+    *converged = res.converged;
+    *iterations = res.iterations;
+    auto* out = new RefTree;
+    out->m = std::move(res.density);
+    out->depth = r->depth;
+    return out;
+  } catch (const std::exception&) {
     return nullptr;
   }
 }

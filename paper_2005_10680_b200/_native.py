@@ -68,6 +68,27 @@ class SquareStats(C.Structure):
 VARIANTS = {"truncmul": 0, "spamm": 1, "hybrid": 2}
 
 
+class PurifyConfig(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("occupation", C.c_int32), ("max_iterations", C.c_int32),
+                ("epsilon", C.c_double), ("idempotency_threshold", C.c_double), ("taus", _dp),
+                ("n_taus", C.c_int32), ("initial_delta", C.c_double), ("deltas", _dp),
+                ("n_deltas", C.c_int32), ("measure_error", C.c_int32)]
+
+
+class RunRecord(C.Structure):
+    _fields_ = [("iteration", C.c_int32), ("status", C.c_int32), ("polynomial", C.c_int32),
+                ("tolerance", C.c_double), ("chosen_tau", C.c_double), ("t_mul", C.c_double),
+                ("t_trunc", C.c_double), ("t_spamm", C.c_double), ("t_cse", C.c_double),
+                ("nnz_in", C.c_int64), ("nnz_mid", C.c_int64), ("nnz_out", C.c_int64),
+                ("nnz_blocks_out", C.c_int64), ("realized_error", C.c_double),
+                ("trace", C.c_double), ("flops", C.c_double)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["status"] = ("ok", "violation", "converged")[self.status]
+        return d
+
+
 class ControlledStats(C.Structure):
     _fields_ = [("tau", C.c_double), ("tau_index", C.c_int32), ("bound", C.c_double),
                 ("cse_seconds", C.c_double), ("spamm_seconds", C.c_double),
@@ -110,6 +131,14 @@ _SIGNATURES = {
     "spg_spamm_with_error_control_to_host": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
                                                        C.c_int64, _i32p, _i32p, _dp, _dp, _i64p,
                                                        _dp, C.POINTER(ControlledStats)]),
+    "spg_matrix_trace": (C.c_int, [_vp, _dp]),
+    "spg_matrix_nnz": (C.c_int, [_vp, _i64p]),
+    "spg_matrix_axpby": (C.c_int, [_vp, C.c_double, _vp, C.c_double, _vp, C.POINTER(_vp)]),
+    "spg_matrix_identity": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "spg_error_budget_geometric": (C.c_int, [C.c_double, C.c_int32, C.c_double, _dp, _dp]),
+    "spg_purify": (C.c_int, [_vp, _vp, C.POINTER(PurifyConfig), C.POINTER(_vp),
+                             C.POINTER(RunRecord), C.c_int32, C.POINTER(C.c_int32),
+                             C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "spg_truncate": (C.c_int, [_vp, _vp, C.c_double, C.POINTER(_vp), _dp, _i64p]),
     "spg_approximate_square": (C.c_int, [_vp, _vp, C.c_int32, C.c_double, _dp, C.c_int32,
                                          C.POINTER(_vp), C.POINTER(SquareStats)]),
@@ -426,6 +455,64 @@ def approximate_square(ctx: Context, x: Matrix, variant: str, delta: float, taus
                                         _ptr(taus, C.c_double), taus.size, C.byref(h),
                                         C.byref(st)))
     return Matrix(ctx, h), st.as_dict()
+
+
+def trace(m: Matrix) -> float:
+    out = C.c_double(0)
+    _check(lib().spg_matrix_trace(m.handle, C.byref(out)))
+    return out.value
+
+
+def nnz(m: Matrix) -> int:
+    out = C.c_int64(0)
+    _check(lib().spg_matrix_nnz(m.handle, C.byref(out)))
+    return out.value
+
+
+def axpby(ctx: Context, alpha: float, a: Matrix, beta: float = 0.0, b: Matrix | None = None):
+    """add(a.scale(alpha), b.scale(beta)) on the device."""
+    h = _vp()
+    _check(lib().spg_matrix_axpby(ctx.handle, alpha, a.handle, beta, b.handle if b else None,
+                                  C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def identity(ctx: Context, n: int, leaf: int) -> Matrix:
+    h = _vp()
+    _check(lib().spg_matrix_identity(ctx.handle, n, leaf, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def error_budget_geometric(epsilon: float, iterations: int, ratio: float = 0.5):
+    d0 = C.c_double(0)
+    deltas = np.empty(max(iterations, 1))
+    _check(lib().spg_error_budget_geometric(epsilon, iterations, ratio, C.byref(d0),
+                                            _ptr(deltas, C.c_double)))
+    return d0.value, deltas[:iterations]
+
+
+def purify(ctx: Context, x0: Matrix, variant: str, occupation: int, epsilon: float = 1e-5,
+           max_iterations: int = 100, taus=None, idempotency_threshold: float = 0.0,
+           budget=None, measure_error: bool = True):
+    """purification.cpp:90-202 on the GPU.  budget = (initial_delta, deltas) or
+    None for ErrorBudget::geometric(epsilon, max_iterations)."""
+    from .inputs import geometric_grid
+    taus = np.ascontiguousarray(geometric_grid() if taus is None else taus, np.float64)
+    if budget is None:
+        budget = error_budget_geometric(epsilon, max_iterations)
+    d0, deltas = budget
+    deltas = np.ascontiguousarray(deltas, np.float64)
+    cfg = PurifyConfig(VARIANTS[variant], occupation, max_iterations, epsilon,
+                       idempotency_threshold, _ptr(taus, C.c_double), taus.size, d0,
+                       _ptr(deltas, C.c_double), deltas.size, int(measure_error))
+    cap = max_iterations + 2
+    log = (RunRecord * cap)()
+    h = _vp()
+    n_log, conv, its = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    _check(lib().spg_purify(ctx.handle, x0.handle, C.byref(cfg), C.byref(h), log, cap,
+                            C.byref(n_log), C.byref(conv), C.byref(its)))
+    return Matrix(ctx, h), [log[i].as_dict() for i in range(min(n_log.value, cap))], \
+        bool(conv.value), its.value
 
 
 # ---------------------------------------------------------------- row shards (SURVEY 8e)

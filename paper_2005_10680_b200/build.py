@@ -30,12 +30,12 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-Wno-deprecated-declarations", "-Xcompiler", "-ffp-contract=off",
     f"-I{INCLUDE}", f"-I{CSRC}",
 ]
-CU_SOURCES = ["norms.cu", "matrix.cu", "cse.cu", "spamm.cu", "synth.cu", "truncate.cu"]
-HEADERS = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
+CU_SOURCES = ["norms.cu", "matrix.cu", "cse.cu", "spamm.cu", "synth.cu", "truncate.cu", "algebra.cu", "purify.cu"]
+HEADERS = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]
 
 CXX = os.environ.get("CXX", "g++")
 DROPIN_SOURCES = ["dropin/quadtree.cpp", "dropin/multiply.cpp", "dropin/error_control.cpp",
-                  "dropin/runtime.cpp"]
+                  "dropin/purification.cpp", "dropin/runtime.cpp"]
 
 
 def _stale(target: Path, deps) -> bool:

@@ -206,6 +206,15 @@ void matrix_destroy(spg_matrix* m);
 // slot_norms[slot] = cached leaf norm (K1 result) for kept slots.
 spg_matrix* matrix_keep_slots(spg_context* ctx, const spg_matrix* x, const double* slot_norms,
                               const uint8_t* keep);
+spg_matrix* controlled_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                               double delta, const double* taus, int n_taus, double* bounds,
+                               spg_controlled_stats* stats);
+// algebra.cu
+double trace_device(spg_context* ctx, const spg_matrix* m);
+int64_t nnz_device(spg_context* ctx, const spg_matrix* m);
+spg_matrix* axpby_device(spg_context* ctx, double alpha, const spg_matrix* a, double beta,
+                         const spg_matrix* b);
+spg_matrix* identity_device(spg_context* ctx, int32_t dimension, int32_t leaf);
 // truncate.cu
 spg_matrix* truncate_device(spg_context* ctx, const spg_matrix* x, double delta,
                             double* removed_norm, int64_t* removed_count);

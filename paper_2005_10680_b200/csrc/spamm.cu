@@ -448,9 +448,6 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   return c;
 }
 
-}  // namespace spg
-
-using namespace spg;
 
 namespace {
 using Clock = std::chrono::steady_clock;
@@ -458,6 +455,44 @@ double seconds_since(Clock::time_point t0) {
   return std::chrono::duration<double>(Clock::now() - t0).count();
 }
 }  // namespace
+
+// spamm_with_error_control (error_control.cpp:203-220) with the context lock
+// held: cse -> select (first k with bound < delta) -> spamm_multiply.
+spg_matrix* controlled_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                               double delta, const double* taus, int n_taus, double* bounds,
+                               spg_controlled_stats* stats) {
+  std::vector<double> local(static_cast<size_t>(n_taus));
+  double* bv = bounds ? bounds : local.data();
+  float cse_ms = 0.0f;
+  const auto t0 = Clock::now();
+  cse_device(ctx, a, b, taus, n_taus, bv, &cse_ms);
+  const double cse_seconds = seconds_since(t0);
+  int32_t k = -1;
+  for (int32_t i = 0; i < n_taus; ++i)
+    if (bv[i] < delta) {
+      k = i;
+      break;
+    }
+  const double tau = k >= 0 ? taus[k] : 0.0;
+  spg_spamm_stats ss{};
+  const auto t1 = Clock::now();
+  spg_matrix* c = spamm_device(ctx, a, b, tau, true, stats ? &ss : nullptr);
+  const double spamm_seconds = seconds_since(t1);
+  if (stats) {
+    stats->tau = tau;
+    stats->tau_index = k;
+    stats->bound = k >= 0 ? bv[k] : 0.0;
+    stats->cse_seconds = cse_seconds;
+    stats->spamm_seconds = spamm_seconds;
+    stats->ms_cse = cse_ms;
+    stats->spamm = ss;
+  }
+  return c;
+}
+
+}  // namespace spg
+
+using namespace spg;
 
 extern "C" {
 
@@ -492,32 +527,7 @@ int spg_spamm_with_error_control(spg_context* ctx, const spg_matrix* a, const sp
   int rc = spg_tolerance_grid_check(taus, n_taus);
   if (rc != SPG_OK) return rc;
   CtxGuard g(ctx);
-  std::vector<double> local(static_cast<size_t>(n_taus));
-  double* bv = bounds ? bounds : local.data();
-  float cse_ms = 0.0f;
-  const auto t0 = Clock::now();
-  cse_device(ctx, a, b, taus, n_taus, bv, &cse_ms);
-  const double cse_seconds = seconds_since(t0);
-  int32_t k = -1;
-  for (int32_t i = 0; i < n_taus; ++i)
-    if (bv[i] < delta) {
-      k = i;
-      break;
-    }
-  const double tau = k >= 0 ? taus[k] : 0.0;
-  spg_spamm_stats ss{};
-  const auto t1 = Clock::now();
-  *c = spamm_device(ctx, a, b, tau, true, stats ? &ss : nullptr);
-  const double spamm_seconds = seconds_since(t1);
-  if (stats) {
-    stats->tau = tau;
-    stats->tau_index = k;
-    stats->bound = k >= 0 ? bv[k] : 0.0;
-    stats->cse_seconds = cse_seconds;
-    stats->spamm_seconds = spamm_seconds;
-    stats->ms_cse = cse_ms;
-    stats->spamm = ss;
-  }
+  *c = controlled_product(ctx, a, b, delta, taus, n_taus, bounds, stats);
   SPG_API_END
 }
 

@@ -18,6 +18,7 @@
 #include "spamm/error_control.hpp"
 #include "spamm/execution.hpp"
 #include "spamm/multiply.hpp"
+#include "spamm/purification.hpp"
 #include "spamm/quadtree.hpp"
 
 using spamm::CoordinateEntry;
@@ -466,6 +467,48 @@ TEST(add_scale, "add and scale follow the reference semantics") {
   CHECK(ok);
   CHECK(spamm::add(a, a.scale(-1.0)).is_zero());
   CHECK(a.scale(0.0).is_zero());
+}
+
+// ---- purification (test_purification.cpp) -------------------------------------
+static QuadTreeMatrix diag_matrix(const std::vector<double>& v, int leaf) {
+  std::vector<CoordinateEntry> e;
+  for (size_t i = 0; i < v.size(); ++i) e.push_back({static_cast<int>(i), static_cast<int>(i), v[i]});
+  return QuadTreeMatrix::from_coordinates(e, static_cast<int>(v.size()), leaf);
+}
+
+TEST(purify_transform, "initial transform maps the spectrum into [0, 1] reversed") {
+  const auto id = QuadTreeMatrix::identity(8, 4);
+  CHECK(bitwise_equal(spamm::initial_transform(id.scale(0.0), {0.0, 2.0}).to_dense(), id.to_dense()));
+  CHECK(spamm::initial_transform(id.scale(2.0), {0.0, 2.0}).is_zero());
+  DenseMatrix expect(3);
+  expect(0, 0) = 1.0;
+  expect(1, 1) = 0.75;
+  CHECK(bitwise_equal(spamm::initial_transform(diag_matrix({-1.0, 0.0, 3.0}, 4), {-1.0, 3.0}).to_dense(), expect));
+  CHECK_THROWS_AS(spamm::initial_transform(id, {1.0, 1.0}), std::invalid_argument);
+}
+
+TEST(purify_sp2, "sp2 selection, budget, and convergence to the projector") {
+  CHECK(spamm::sp2_step(diag_matrix({0.9, 0.3}, 2), 1).polynomial == spamm::Sp2Polynomial::square);
+  CHECK(spamm::sp2_step(diag_matrix({1.5, 0.5}, 2), 2).polynomial ==
+        spamm::Sp2Polynomial::trace_correcting);
+  const auto b = spamm::ErrorBudget::geometric(1e-5, 40);
+  CHECK(b.initial_delta == 5e-6 && approx(b.total(), 1e-5, 1e-12));
+  DenseMatrix expect(4);
+  expect(0, 0) = 1.0;
+  expect(1, 1) = 1.0;
+  for (auto v : {spamm::Variant::truncmul, spamm::Variant::spamm, spamm::Variant::hybrid}) {
+    spamm::PurificationConfig cfg;
+    cfg.variant = v;
+    cfg.occupation = 2;
+    cfg.epsilon = 1e-6;
+    const auto r = spamm::purify(diag_matrix({0.9, 0.8, 0.2, 0.1}, 4), cfg);
+    CHECK(r.converged);
+    CHECK(diff_frob(r.density.to_dense(), expect) < 1e-6);
+    CHECK(!r.log.empty() && r.log.back().status == "converged");
+  }
+  spamm::PurificationConfig bad;
+  bad.occupation = 0;
+  CHECK_THROWS_AS(spamm::purify(diag_matrix({1.0, 0.0}, 2), bad), std::invalid_argument);
 }
 
 int main() {
