@@ -311,6 +311,10 @@ def run_ours(args, dist):
     }
     if clk:
         out["clocks"] = clk
+    if not sharded:  # SURVEY 8a parity audit: how close the decisions are to ties
+        ties, cands = nat.parity_audit(ctx, A, A, st["tau"], 4)
+        out["parity_audit"] = {"near_ties_4ulp": ties, "candidates": cands,
+                               "bound_margin": (w.delta - st["bound"]) / w.delta}
 
     host = None
     if not args.no_e2e and not sharded:

@@ -157,6 +157,12 @@ int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
 int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                   int64_t* count, int32_t* triples, int64_t capacity);
 
+/* Parity audit: of all candidate leaf products (non-null
+ * A(i,k) x B(k,j)), how many have |fl(nA*nB) - tau| <= ulps * ulp(tau) --
+ * the decisions a one-ulp norm difference could flip. */
+int spg_parity_audit(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                     int32_t ulps, int64_t* near_ties, int64_t* candidates);
+
 /* ---- callers of the hot path (SURVEY.md 8f "next" row 1) ----------------- */
 /* truncate (error_control.hpp:59-62, error_control.cpp:174-201): remove whole
  * leaves greedily in ascending (norm, row-major position) order while the

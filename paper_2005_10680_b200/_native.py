@@ -131,6 +131,7 @@ _SIGNATURES = {
     "spg_spamm_with_error_control_to_host": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp, C.c_int32,
                                                        C.c_int64, _i32p, _i32p, _dp, _dp, _i64p,
                                                        _dp, C.POINTER(ControlledStats)]),
+    "spg_parity_audit": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, _i64p, _i64p]),
     "spg_matrix_trace": (C.c_int, [_vp, _dp]),
     "spg_matrix_nnz": (C.c_int, [_vp, _i64p]),
     "spg_matrix_axpby": (C.c_int, [_vp, C.c_double, _vp, C.c_double, _vp, C.POINTER(_vp)]),
@@ -455,6 +456,14 @@ def approximate_square(ctx: Context, x: Matrix, variant: str, delta: float, taus
                                         _ptr(taus, C.c_double), taus.size, C.byref(h),
                                         C.byref(st)))
     return Matrix(ctx, h), st.as_dict()
+
+
+def parity_audit(ctx: Context, a: Matrix, b: Matrix, tau: float, ulps: int = 4):
+    """(near_ties, candidates): candidate products within `ulps` ulp of tau."""
+    t, c = C.c_int64(0), C.c_int64(0)
+    _check(lib().spg_parity_audit(ctx.handle, a.handle, b.handle, tau, ulps, C.byref(t),
+                                  C.byref(c)))
+    return t.value, c.value
 
 
 def trace(m: Matrix) -> float:

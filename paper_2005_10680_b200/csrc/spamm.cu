@@ -15,6 +15,7 @@
 // >= 1 survivor; its norm follows block_norm (K1); all-zero sums collapse to
 // null (make_leaf); inner norms follow combine_child_norms (K2).
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
@@ -75,6 +76,39 @@ __global__ void count_products(const int32_t* __restrict__ colA, const int32_t* 
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   out[k] = static_cast<int64_t>(colA[k]) * rowB[k];
+}
+
+// Parity audit (SURVEY.md 8a "Audit"): candidate leaf products whose norm
+// product lies within `ulps` units in the last place of tau -- the pairs
+// whose skip decision a 1-ulp difference in a norm could flip.
+__global__ void near_tie_count(const int32_t* __restrict__ I, const int32_t* __restrict__ K,
+                               const int32_t* __restrict__ J, int64_t n,
+                               const double* __restrict__ pa, const double* __restrict__ pb,
+                               double tau, double window, unsigned long long* __restrict__ ties,
+                               unsigned long long* __restrict__ cands) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long t = 0, c = 0;
+  if (p < n) {
+    const uint32_t i0 = 2u * I[p], k0 = 2u * K[p], j0 = 2u * J[p];
+#pragma unroll
+    for (int code = 0; code < 8; ++code) {
+      const uint32_t r = code >> 2, cc = (code >> 1) & 1, h = code & 1;
+      const double na = pa[morton2(i0 + r, k0 + h)];
+      const double nb = pb[morton2(k0 + h, j0 + cc)];
+      if (na < 0.0 || nb < 0.0) continue;
+      ++c;
+      const double prod = __dmul_rn(na, nb);
+      if (fabs(prod - tau) <= window) ++t;
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    t += __shfl_down_sync(0xffffffffu, t, off);
+    c += __shfl_down_sync(0xffffffffu, c, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (t) atomicAdd(ties, t);
+    if (c) atomicAdd(cands, c);
+  }
 }
 
 struct TaskList {
@@ -241,6 +275,10 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
   }
   if (L == 64 && gemm_variant() == 6) {  // 4 warps x 32x32, KC=16, 4 stages, 3 CTAs/SM
     launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    return;
+  }
+  if (L == 64 && gemm_variant() == 8) {  // 4 warps x 32x32, KC=16, 3 stages, 3 CTAs/SM
+    launch_dmma<64, 16, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 7) {  // 4 warps x 32x32, KC=16, 6 stages, 2 CTAs/SM
@@ -585,6 +623,50 @@ int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
     stats->ms_cse = cse_ms;
     stats->spamm = ss;
   }
+  SPG_API_END
+}
+
+int spg_parity_audit(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                     int32_t ulps, int64_t* near_ties, int64_t* candidates) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !near_ties || !candidates) fail(SPG_EINVAL, "null argument");
+  if (a->dimension != b->dimension || a->leaf != b->leaf)
+    fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
+  CtxGuard g(ctx);
+  *near_ties = 0;
+  *candidates = 0;
+  const int d = a->depth;
+  const double window = ulps * (std::nextafter(tau, 2.0 * tau + 1.0) - tau);
+  if (d == 0) {
+    double na = -1, nb = -1;
+    SPG_CUDA(cudaMemcpy(&na, a->pyramid, 8, cudaMemcpyDeviceToHost));
+    SPG_CUDA(cudaMemcpy(&nb, b->pyramid, 8, cudaMemcpyDeviceToHost));
+    if (na >= 0 && nb >= 0) {
+      *candidates = 1;
+      volatile double p = na * nb;
+      *near_ties = std::fabs(p - tau) <= window;
+    }
+    return SPG_OK;
+  }
+  TripleList cur = root_list<KeepRule::kExact>(ctx, a, b, 0.0);
+  for (int l = 0; l < d - 1 && cur.n > 0; ++l) {
+    TripleList next = expand_level<KeepRule::kExact>(ctx, cur, a->pyramid + level_offset(l + 1),
+                                                     b->pyramid + level_offset(l + 1), 0.0);
+    cur = std::move(next);
+  }
+  DevBuf<unsigned long long> cnt(2, ctx);
+  SPG_CUDA(cudaMemsetAsync(cnt.get(), 0, 16, ctx->stream));
+  if (cur.n) {
+    near_tie_count<<<grid_for(cur.n, 256), 256, 0, ctx->stream>>>(
+        cur.I.get(), cur.K.get(), cur.J.get(), cur.n, a->pyramid + level_offset(d),
+        b->pyramid + level_offset(d), tau, window, cnt.get(), cnt.get() + 1);
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  unsigned long long h[2] = {0, 0};
+  SPG_CUDA(cudaMemcpyAsync(h, cnt.get(), 16, cudaMemcpyDeviceToHost, ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *near_ties = static_cast<int64_t>(h[0]);
+  *candidates = static_cast<int64_t>(h[1]);
   SPG_API_END
 }
 

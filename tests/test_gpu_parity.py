@@ -93,7 +93,7 @@ def _random_case(rng, n, L, fill, decay):
     return d
 
 
-@pytest.mark.parametrize("L", [2, 4, 8, 16, 32, 64, 128])
+@pytest.mark.parametrize("L", [2, 3, 4, 8, 12, 16, 24, 32, 48, 64, 128])
 def test_random_vs_oracle_all_leaf_sizes(ctx, port, L):
     """Every GEMM instantiation (generic, DMMA L=32/64/128) and ragged sizes."""
     from paper_2005_10680_b200 import _native as nat
@@ -171,3 +171,18 @@ def test_streamed_to_host_equals_device_product(ctx, L):
         nat.spamm_with_error_control_to_host(
             ctx, A, A, 1e-6, taus, out=(np.empty(1, np.int32), np.empty(1, np.int32),
                                         np.empty((1, L * L)), np.empty(1)))
+
+
+def test_parity_audit_counts(ctx, port):
+    """The near-tie audit counts candidates exactly (oracle candidate count) and
+    finds a product placed exactly on tau."""
+    from paper_2005_10680_b200 import _native as nat
+    rows, cols, pay = nat.synth_chain_host(1024, 32, 20.0, 3, 1e-10)
+    A = nat.upload(ctx, 1024, 32, rows, cols, pay)
+    t = port.build(1024, 32, rows, cols, pay)
+    ties, cands = nat.parity_audit(ctx, A, A, 1e-6, 4)
+    assert cands == port._cand(t.h, t.h)
+    _, _, _, norms = A.download(payload=False)
+    tau = float(norms[0] * norms[0])  # the (0,0,0) leaf product itself
+    ties, _ = nat.parity_audit(ctx, A, A, tau, 0)
+    assert ties >= 1
