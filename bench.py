@@ -71,27 +71,36 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.device = self.local_rank
         self.pg = None
+        self.backend = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-            if backend == "nccl":
-                torch.cuda.set_device(self.local_rank)
-            dist.init_process_group(backend)
+            # SPG_DIST_BACKEND=gloo: host-side collectives (lets a 1-GPU box run
+            # the sharded path with ranks time-sharing the device; no rank's
+            # kernels ever wait on another rank's)
+            self.backend = os.environ.get("SPG_DIST_BACKEND") or (
+                "nccl" if torch.cuda.is_available() else "gloo")
+            if torch.cuda.is_available():
+                self.device = self.local_rank % torch.cuda.device_count()
+                torch.cuda.set_device(self.device)
+            dist.init_process_group(self.backend)
             self.pg = dist
 
     def barrier(self):
         if self.pg:
             self.pg.barrier()
 
+    def _dev(self):
+        return "cuda" if self.backend == "nccl" else "cpu"
+
     def max(self, x: float) -> float:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64,
-                         device="cuda" if torch.cuda.is_available() else "cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=self._dev())
         self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
         return float(t.item())
 
@@ -99,18 +108,21 @@ class Dist:
         if not self.pg:
             return x
         import torch
-        t = torch.tensor([x], dtype=torch.float64,
-                         device="cuda" if torch.cuda.is_available() else "cpu")
+        t = torch.tensor([x], dtype=torch.float64, device=self._dev())
         self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
         return float(t.item())
 
     def all_gather_np(self, arr):
         """NCCL all-gather of a small host array -> (world, *arr.shape)."""
         import torch
-        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
-        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        self.pg.all_gather_into_tensor(out, t)
-        return out.cpu().numpy()
+        t = torch.from_numpy(np.ascontiguousarray(arr)).to(self._dev())
+        if self.backend == "nccl":
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            self.pg.all_gather_into_tensor(out, t)
+            return out.cpu().numpy()
+        parts = [torch.empty_like(t) for _ in range(self.world)]
+        self.pg.all_gather(parts, t)
+        return torch.stack(parts).numpy()
 
     def close(self):
         if self.pg:
@@ -213,8 +225,8 @@ def run_ours(args, dist):
     from paper_2005_10680_b200.sharded import controlled_product_shard
 
     w = CONFIGS[args.workload]
-    torch.cuda.set_device(dist.local_rank)
-    ctx = nat.Context(dist.local_rank)
+    torch.cuda.set_device(dist.device)
+    ctx = nat.Context(dist.device)
     stream = torch.cuda.ExternalStream(ctx.stream)
     A = make_matrix(nat, ctx, w)
     taus = log_grid(w.n_taus)
@@ -238,7 +250,7 @@ def run_ours(args, dist):
         del C
     ctx.synchronize()
     dist.barrier()
-    clocks = Clocks(dist.local_rank)
+    clocks = Clocks(dist.device)
     clocks.start()
     launches0 = ctx.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -285,8 +297,9 @@ def run_ours(args, dist):
         "config": {"workload": w.name, "n": w.n, "leaf": w.leaf, "ell": w.ell,
                    "density": w.density, "delta": w.delta, "n_taus": w.n_taus,
                    "tau_grid": "log-spaced [1e-12, 1e-2]", "drop": w.drop,
-                   "parallelism": (f"row-shards x{dist.world} (level {level}), NCCL all-gather of "
-                                   f"level-{level} CSE vectors" if sharded else
+                   "parallelism": (f"row-shards x{dist.world} (level {level}), "
+                                   f"{dist.backend} all-gather of level-{level} CSE vectors"
+                                   if sharded else
                                    f"replicas x{dist.world}" if dist.world > 1 else "single"),
                    "l2": "no flush: each step streams 8.6 GB of leaves (>> 126 MB L2)"},
         "pct_peak": round(100.0 * value / DMMA_PEAK_TFLOPS, 2),
@@ -413,7 +426,7 @@ def run_reference(args, dist):
     w = CONFIGS[args.workload]
     # Input generation (not timed, not on the measured path): the same seeded
     # matrix bits the GPU arm uses, produced by the device generator.
-    ctx = nat.Context(dist.local_rank)
+    ctx = nat.Context(dist.device)
     A = make_matrix(nat, ctx, w)
     taus = log_grid(w.n_taus)
     rows, cols, pay, _ = A.download(payload=True)

@@ -63,11 +63,15 @@ __global__ void make_pairs(const uint64_t* __restrict__ keys, int64_t n, int kbi
   pairs[t] = make_int2(gridA[morton2(i, k)], gridB[morton2(k, j)]);
 }
 
+// leaves of a matrix per block column (use_col) or row; with use_col, only
+// leaves whose block row lies in [row_lo, row_hi) count (a row shard's A)
 __global__ void count_by_index(const uint64_t* __restrict__ keys, int64_t n, bool use_col,
-                               int32_t* __restrict__ counts) {
+                               uint32_t row_lo, uint32_t row_hi, int32_t* __restrict__ counts) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const uint32_t idx = use_col ? morton_col(keys[t]) : morton_row(keys[t]);
+  const uint32_t r = morton_row(keys[t]);
+  if (use_col && (r < row_lo || r >= row_hi)) return;
+  const uint32_t idx = use_col ? morton_col(keys[t]) : r;
   atomicAdd(counts + idx, 1);
 }
 
@@ -191,20 +195,23 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
   return tl;
 }
 
-int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix* b) {
+int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                         Shard sh = {}) {
   const int nb = 1 << a->depth;
+  const uint32_t rows_per = static_cast<uint32_t>(nb >> sh.level);
+  const uint32_t row_lo = rows_per * sh.index, row_hi = row_lo + rows_per;
   DevBuf<int32_t> colA(nb, ctx), rowB(nb, ctx);
   DevBuf<int64_t> prod(nb, ctx), total(1, ctx);
   SPG_CUDA(cudaMemsetAsync(colA.get(), 0, nb * sizeof(int32_t), ctx->stream));
   SPG_CUDA(cudaMemsetAsync(rowB.get(), 0, nb * sizeof(int32_t), ctx->stream));
   if (a->nnzb) {
     count_by_index<<<grid_for(a->nnzb, 256), 256, 0, ctx->stream>>>(a->keys, a->nnzb, true,
-                                                                    colA.get());
+                                                                    row_lo, row_hi, colA.get());
     SPG_CHECK_LAUNCH(ctx);
   }
   if (b->nnzb) {
-    count_by_index<<<grid_for(b->nnzb, 256), 256, 0, ctx->stream>>>(b->keys, b->nnzb, false,
-                                                                    rowB.get());
+    count_by_index<<<grid_for(b->nnzb, 256), 256, 0, ctx->stream>>>(b->keys, b->nnzb, false, 0,
+                                                                    0, rowB.get());
     SPG_CHECK_LAUNCH(ctx);
   }
   count_products<<<grid_for(nb, 256), 256, 0, ctx->stream>>>(colA.get(), rowB.get(), nb,
@@ -481,7 +488,7 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     SPG_CUDA(cudaEventElapsedTime(&stats->ms_tasklist, ctx->ev[2], ctx->ev[3]));
     SPG_CUDA(cudaEventElapsedTime(&stats->ms_gemm, ctx->ev[3], ctx->ev[4]));
     SPG_CUDA(cudaEventElapsedTime(&stats->ms_finalize, ctx->ev[4], ctx->ev[5]));
-    stats->candidates = count_candidates(ctx, a, b);
+    stats->candidates = count_candidates(ctx, a, b, shard);
   }
   return c;
 }

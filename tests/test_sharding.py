@@ -117,6 +117,8 @@ def test_gpu_shards_reproduce_single_gpu(ctx, level):
         for i in range(len(rs)):
             got[(rs[i], cs[i])] = (ps[i], ns[i])
     assert total == st["survivors"]
+    assert sum(nat.spamm_shard(ctx, A, A, tau, level, s)[1]["candidates"]
+               for s in range(2 ** level)) == st["candidates"]
     assert len(got) == len(r)
     for i in range(len(r)):
         gp, gn = got[(r[i], c[i])]
