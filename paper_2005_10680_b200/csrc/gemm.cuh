@@ -58,14 +58,14 @@ struct DmmaGemmCfg {
   static constexpr int TM = WM / 8;
   static constexpr int TN = WN / 8;
   static constexpr size_t kSmemBytes = sizeof(double) * NSTAGE * STAGE;
-  static_assert(kWarps == 4 || kWarps == 8, "4 or 8 warps per CTA");
+  static_assert(kWarps == 1 || kWarps == 2 || kWarps == 4 || kWarps == 8, "1-8 warps per CTA");
   static_assert(AS % 16 == 4 && BS % 16 == 4, "bank-conflict-free strides");
   static_assert(L % KC == 0 && KC % 4 == 0, "k chunking");
 };
 
 template <int L, int KC, int WM, int WN, int NSTAGE>
 __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
-                                  (L > 64) ? 1 : ((L / WM) * (L / WN) == 4 ? 3 : 2))
+                                  (L > 64) ? 1 : ((L / WM) * (L / WN) <= 4 ? 3 : 2))
     leaf_gemm_dmma(const double* __restrict__ A, const double* __restrict__ B,
                    const int2* __restrict__ pairs, const int64_t* __restrict__ out_offset,
                    int64_t n_out, double* __restrict__ C) {

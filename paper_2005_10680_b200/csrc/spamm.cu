@@ -293,9 +293,18 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
     return;
   }
   switch (L) {
-    case 32:
-      launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    case 32: {
+      static const int v32 = [] {
+        const char* e = std::getenv("SPG_GEMM32");  // developer switch for the L=32 tiling
+        return e ? std::atoi(e) : 2;
+      }();
+      if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
       break;
+    }
     case 64:
       launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
       break;
