@@ -264,6 +264,38 @@ int spg_matrix_top_norms(const spg_matrix* m, int32_t levels, double* out);
 int spg_spamm_shard(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                     int32_t level, int32_t shard, spg_matrix** c, spg_spamm_stats* stats);
 
+/* ---- B resident in host memory, streamed in panels (SURVEY.md 8e, configs
+ * 4/5: operands larger than one GPU's HBM) -----------------------------------
+ * The leaves of B are given sorted by block row (ties in any order) and stay
+ * in the caller's host buffer, which must outlive the stream object.  Panel
+ * p holds block rows [p*panel_block_rows, (p+1)*panel_block_rows).  Creation
+ * streams the panels through the leaf-norm kernel once to build B's norm
+ * pyramid; the products then copy each panel (double-buffered, overlapping
+ * the GEMM of the previous one) and continue every output block's
+ * accumulator over the panel's k range.  Results are bitwise identical to
+ * the same call with B resident (spg_matrix_upload + spg_spamm / spg_cse).
+ * register_host != 0 page-locks the caller's buffer for the stream's
+ * lifetime (asynchronous copies); 0 leaves it as is. */
+typedef struct spg_bstream spg_bstream;
+int spg_bstream_create(spg_context* ctx, int32_t dimension, int32_t leaf_size, int64_t n_leaves,
+                       const int32_t* block_rows, const int32_t* block_cols,
+                       const double* payload, int32_t panel_block_rows, int32_t register_host,
+                       spg_bstream** out);
+/* B's norm-only matrix: valid for spg_cse, spg_matrix_get_info,
+ * spg_matrix_level_norms, spg_matrix_download without payload; SPG_EINVAL
+ * where leaf values are needed. Owned by the stream object. */
+int spg_bstream_matrix(const spg_bstream* bs, const spg_matrix** norms);
+int spg_bstream_panels(const spg_bstream* bs, int32_t* n_panels, int64_t* max_panel_leaves);
+void spg_bstream_free(spg_bstream* bs);
+/* spamm_multiply (multiply.cpp:109-116) with B streamed from host memory. */
+int spg_spamm_streamed(spg_context* ctx, const spg_matrix* a, const spg_bstream* b, double tau,
+                       spg_matrix** c, spg_spamm_stats* stats);
+/* spamm_with_error_control (error_control.cpp:203-220) with B streamed. */
+int spg_spamm_with_error_control_streamed(spg_context* ctx, const spg_matrix* a,
+                                          const spg_bstream* b, double delta, const double* taus,
+                                          int32_t n_taus, spg_matrix** c, double* bounds,
+                                          spg_controlled_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

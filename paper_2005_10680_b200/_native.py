@@ -148,6 +148,16 @@ _SIGNATURES = {
     "spg_matrix_top_norms": (C.c_int, [_vp, C.c_int32, _dp]),
     "spg_spamm_shard": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32,
                                   C.POINTER(_vp), C.POINTER(SpammStats)]),
+    "spg_bstream_create": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p, _dp,
+                                     C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "spg_bstream_matrix": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "spg_bstream_panels": (C.c_int, [_vp, C.POINTER(C.c_int32), _i64p]),
+    "spg_bstream_free": (None, [_vp]),
+    "spg_spamm_streamed": (C.c_int, [_vp, _vp, _vp, C.c_double, C.POINTER(_vp),
+                                     C.POINTER(SpammStats)]),
+    "spg_spamm_with_error_control_streamed": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp,
+                                                        C.c_int32, C.POINTER(_vp), _dp,
+                                                        C.POINTER(ControlledStats)]),
     "spg_synth_chain_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double,
                                        C.c_int64, _i32p, _i32p, _dp, _i64p]),
     "spg_synth_cluster_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
@@ -309,7 +319,8 @@ class Matrix:
 
     def free(self):
         if getattr(self, "_h", None):
-            lib().spg_matrix_free(self._h)
+            if not getattr(self, "_borrowed", False):
+                lib().spg_matrix_free(self._h)
             self._h = None
 
     def __del__(self):
@@ -560,6 +571,86 @@ def spamm_shard(ctx: Context, a: Matrix, b: Matrix, tau: float, level: int, shar
     _check(lib().spg_spamm_shard(ctx.handle, a.handle, b.handle, tau, level, shard, C.byref(h),
                                  C.byref(st)))
     return Matrix(ctx, h), st.as_dict()
+
+
+# ------------------------------------------------- B streamed from host memory
+class BStream:
+    """B kept in host memory and streamed to the GPU in panels of block rows
+    (spg_bstream_*).  Leaves must be sorted by block row; the payload array
+    is referenced (not copied) for the object's lifetime."""
+
+    def __init__(self, ctx: Context, dimension: int, leaf_size: int, rows, cols, payload,
+                 panel_block_rows: int, register_host: bool = True):
+        self.ctx = ctx
+        self._rows = np.ascontiguousarray(rows, np.int32)
+        self._cols = np.ascontiguousarray(cols, np.int32)
+        if isinstance(payload, np.ndarray):
+            self._payload = np.ascontiguousarray(payload, np.float64)
+            pay_ptr = _ptr(self._payload, C.c_double)
+        else:  # a (pinned) torch CPU tensor
+            self._payload = payload
+            pay_ptr = C.cast(C.c_void_p(payload.data_ptr()), C.POINTER(C.c_double))
+        n = self._rows.shape[0]
+        self._h = _vp()
+        _check(lib().spg_bstream_create(ctx.handle, dimension, leaf_size, n,
+                                        _ptr(self._rows, C.c_int32), _ptr(self._cols, C.c_int32),
+                                        pay_ptr, panel_block_rows, int(register_host),
+                                        C.byref(self._h)))
+        m = _vp()
+        _check(lib().spg_bstream_matrix(self._h, C.byref(m)))
+        self.norms = Matrix(ctx, m)
+        self.norms._borrowed = True
+        self.norms._owner = self  # keeps the stream (and its payload) alive
+
+    @property
+    def handle(self):
+        return self._h
+
+    def panels(self):
+        n = C.c_int32(0)
+        mx = C.c_int64(0)
+        _check(lib().spg_bstream_panels(self._h, C.byref(n), C.byref(mx)))
+        return n.value, mx.value
+
+    def free(self):
+        if getattr(self, "_h", None):
+            self.norms._h = None
+            lib().spg_bstream_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        if sys is None or sys.is_finalizing():
+            return
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sort_by_block_row(rows, cols, payload):
+    """Leaves reordered by (block row, block column) for BStream."""
+    order = np.lexsort((np.asarray(cols), np.asarray(rows)))
+    return (np.asarray(rows)[order], np.asarray(cols)[order],
+            np.ascontiguousarray(np.asarray(payload)[order]))
+
+
+def spamm_streamed(ctx: Context, a: Matrix, b: BStream, tau: float):
+    h = _vp()
+    st = SpammStats()
+    _check(lib().spg_spamm_streamed(ctx.handle, a.handle, b.handle, tau, C.byref(h),
+                                    C.byref(st)))
+    return Matrix(ctx, h), st.as_dict()
+
+
+def spamm_with_error_control_streamed(ctx: Context, a: Matrix, b: BStream, delta: float, taus):
+    taus = np.ascontiguousarray(taus, np.float64)
+    bounds = np.empty(taus.size, np.float64)
+    h = _vp()
+    st = ControlledStats()
+    _check(lib().spg_spamm_with_error_control_streamed(
+        ctx.handle, a.handle, b.handle, delta, _ptr(taus, C.c_double), taus.size, C.byref(h),
+        _ptr(bounds, C.c_double), C.byref(st)))
+    return Matrix(ctx, h), st.as_dict(), bounds
 
 
 # ---------------------------------------------------------------- synthetic inputs

@@ -80,6 +80,7 @@ __global__ void axpby_blocks(const uint64_t* __restrict__ keys, int64_t n, doubl
 }  // namespace
 
 double trace_device(spg_context* ctx, const spg_matrix* m) {
+  require_payload(m);
   const int32_t nb = 1 << m->depth;
   DevBuf<double> t(nb, ctx);
   diag_leaf_traces<<<grid_for(nb, 128), 128, 0, ctx->stream>>>(m->grid_slot, nb, m->payload,
@@ -99,6 +100,7 @@ double trace_device(spg_context* ctx, const spg_matrix* m) {
 }
 
 int64_t nnz_device(spg_context* ctx, const spg_matrix* m) {
+  require_payload(m);
   if (m->nnzb == 0) return 0;
   DevBuf<unsigned long long> total(1, ctx);
   SPG_CUDA(cudaMemsetAsync(total.get(), 0, sizeof(unsigned long long), ctx->stream));
@@ -114,6 +116,8 @@ int64_t nnz_device(spg_context* ctx, const spg_matrix* m) {
 
 spg_matrix* axpby_device(spg_context* ctx, double alpha, const spg_matrix* a, double beta,
                          const spg_matrix* b) {
+  require_payload(a);
+  require_payload(b);
   if (b && (a->dimension != b->dimension || a->leaf != b->leaf))
     fail(SPG_EINVAL, "add: dimension or leaf size mismatch");
   // QuadTreeMatrix::scale(0) is the zero matrix (quadtree.cpp:249-252)

@@ -97,6 +97,21 @@ struct spg_matrix {
   int32_t* grid_slot = nullptr; // 4^depth
   double* pyramid = nullptr;    // sum_l 4^l
   double frob = 0.0;
+  bool norms_only = false;      // norms of a host-resident B (spg_bstream): no payload
+};
+
+// B kept in host memory and streamed to the GPU in panels of block rows
+// (SURVEY.md 8e, configs 4/5): leaves sorted by block row, panel p = block
+// rows [panel_row[p], panel_row[p+1]) = leaves [panel_leaf[p], panel_leaf[p+1]).
+// `norms` is a norm-only matrix whose grid_slot holds the sorted leaf index.
+struct spg_bstream {
+  spg_context* ctx = nullptr;
+  spg_matrix* norms = nullptr;
+  const double* host_payload = nullptr;
+  bool registered = false;  // host payload page-locked by spg_bstream_create
+  std::vector<int32_t> panel_row;
+  std::vector<int64_t> panel_leaf;
+  int64_t max_panel_leaves = 0;
 };
 
 namespace spg {
@@ -243,6 +258,21 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
                          HostOut* host = nullptr);
 
 int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
+
+// the product with B streamed panel by panel from host memory; C identical
+// (bitwise) to spamm_device with B resident
+spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const spg_bstream* b,
+                                  double tau, spg_spamm_stats* stats);
+// matrix.cu: norm-only matrix from per-leaf norms (slot = leaf index)
+spg_matrix* matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf,
+                                   int64_t n_leaves, const int32_t* d_rows,
+                                   const int32_t* d_cols, const double* d_norms,
+                                   const uint8_t* d_nonzero);
+
+inline void require_payload(const spg_matrix* m) {
+  if (m && m->norms_only)
+    fail(SPG_EINVAL, "matrix holds the norms of a host-resident B only (use spg_spamm_streamed)");
+}
 
 // SPG_TRACE=1: synchronising host-side phase timer printed to stderr
 // (diagnostics only; off by default, never used for reported numbers).

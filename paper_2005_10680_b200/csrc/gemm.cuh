@@ -68,7 +68,8 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
                                   (L > 64) ? 1 : ((L / WM) * (L / WN) <= 4 ? 3 : 2))
     leaf_gemm_dmma(const double* __restrict__ A, const double* __restrict__ B,
                    const int2* __restrict__ pairs, const int64_t* __restrict__ out_offset,
-                   int64_t n_out, double* __restrict__ C) {
+                   int64_t n_out, double* __restrict__ C, const int64_t* __restrict__ out_end,
+                   int accumulate) {
   using Cfg = DmmaGemmCfg<L, KC, WM, WN, NSTAGE>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
@@ -80,8 +81,11 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
   constexpr int64_t LL = static_cast<int64_t>(L) * L;
 
   for (int64_t o = blockIdx.x; o < n_out; o += gridDim.x) {
+    // products of block o: pairs[beg, end); a B-panel launch passes its own
+    // end[] and continues the accumulator stored by the previous panel
     const int64_t beg = out_offset[o];
-    const int64_t nsteps = (out_offset[o + 1] - beg) * Cfg::CHUNKS;
+    const int64_t nsteps = ((out_end ? out_end[o] : out_offset[o + 1]) - beg) * Cfg::CHUNKS;
+    if (nsteps == 0) continue;  // uniform per CTA
 
     auto load_stage = [&](int2 pr, int64_t step, int stage) {
       const int c = static_cast<int>(step % Cfg::CHUNKS);
@@ -110,7 +114,12 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
 #pragma unroll
     for (int i = 0; i < Cfg::TM; ++i)
 #pragma unroll
-      for (int j = 0; j < Cfg::TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < Cfg::TN; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          acc[i][j][e] = accumulate ? C[o * LL + static_cast<int64_t>(n0 + 8 * j + perm8(2 * t + e)) * L +
+                                        m0 + 8 * i + pg]
+                                    : 0.0;
 
 #pragma unroll
     for (int s = 0; s < NSTAGE - 1; ++s) {
@@ -164,13 +173,15 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
 static __global__ void leaf_gemm_generic(const double* __restrict__ A, const double* __restrict__ B,
                                   const int2* __restrict__ pairs,
                                   const int64_t* __restrict__ out_offset, int64_t n_out, int L,
-                                  double* __restrict__ C) {
+                                  double* __restrict__ C, const int64_t* __restrict__ out_end,
+                                  int accumulate) {
   const int64_t LL = static_cast<int64_t>(L) * L;
   for (int64_t o = blockIdx.x; o < n_out; o += gridDim.x) {
-    const int64_t beg = out_offset[o], end = out_offset[o + 1];
+    const int64_t beg = out_offset[o], end = out_end ? out_end[o] : out_offset[o + 1];
+    if (beg == end) continue;
     for (int64_t e = threadIdx.x; e < LL; e += blockDim.x) {
       const int64_t i = e % L, j = e / L;
-      double acc = 0.0;
+      double acc = accumulate ? C[o * LL + e] : 0.0;
       for (int64_t s = beg; s < end; ++s) {
         const int2 pr = pairs[s];
         const double* a = A + pr.x * LL + i;

@@ -287,6 +287,39 @@ spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32
   return m.release();
 }
 
+spg_matrix* matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf,
+                                   int64_t n_leaves, const int32_t* d_rows,
+                                   const int32_t* d_cols, const double* d_norms,
+                                   const uint8_t* d_nonzero) {
+  std::unique_ptr<spg_matrix, void (*)(spg_matrix*)> m(new_matrix(ctx, dimension, leaf),
+                                                       matrix_destroy);
+  m->norms_only = true;
+  m->n_slots = n_leaves;
+  if (n_leaves > (int64_t(1) << 31) - 1) fail(SPG_EINVAL, "too many leaves");
+  const int32_t nb_logical = (dimension + leaf - 1) / leaf;
+  DevBuf<int> flags(1, ctx);
+  SPG_CUDA(cudaMemsetAsync(flags.get(), 0, sizeof(int), ctx->stream));
+  if (n_leaves) {
+    scatter_leaves<<<grid_for(n_leaves, 256), 256, 0, ctx->stream>>>(
+        d_rows, d_cols, n_leaves, nb_logical, m->grid_slot, flags.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  int h_flags = 0;
+  SPG_CUDA(cudaMemcpyAsync(&h_flags, flags.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h_flags & 1) fail(SPG_ERANGE, "block coordinate outside the matrix dimension");
+  if (h_flags & 2) fail(SPG_EINVAL, "duplicate block coordinate");
+  build_pyramid(ctx, m.get(), d_norms, d_nonzero);
+  compact_leaves(ctx, m.get());
+  double root = -1.0;
+  SPG_CUDA(cudaMemcpyAsync(&root, m->pyramid, sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  m->frob = root < 0.0 ? 0.0 : root;
+  return m.release();
+}
+
 spg_matrix* matrix_keep_slots(spg_context* ctx, const spg_matrix* x, const double* slot_norms,
                               const uint8_t* keep) {
   std::unique_ptr<spg_matrix, void (*)(spg_matrix*)> m(new_matrix(ctx, x->dimension, x->leaf),
@@ -514,6 +547,7 @@ int spg_matrix_download(const spg_matrix* m, int32_t* block_rows, int32_t* block
                         double* payload, double* norms) {
   SPG_API_BEGIN
   if (!m) fail(SPG_EINVAL, "null matrix");
+  if (payload) require_payload(m);
   spg_context* ctx = m->ctx;
   CtxGuard g(ctx);
   if (m->nnzb == 0) return SPG_OK;
@@ -556,6 +590,7 @@ int spg_matrix_download(const spg_matrix* m, int32_t* block_rows, int32_t* block
 int spg_matrix_to_dense(const spg_matrix* m, double* dense) {
   SPG_API_BEGIN
   if (!m || !dense) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
   const int64_t n = m->dimension, L = m->leaf, elems = L * L;
   std::vector<int32_t> rows(static_cast<size_t>(m->nnzb)), cols(static_cast<size_t>(m->nnzb));
   std::vector<double> payload(static_cast<size_t>(m->nnzb * elems));

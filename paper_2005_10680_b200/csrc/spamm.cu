@@ -227,13 +227,15 @@ int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix
 
 template <int L, int KC, int WM, int WN, int NSTAGE>
 void launch_dmma(spg_context* ctx, const double* A, const double* B, const int2* pairs,
-                 const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st) {
+                 const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st,
+                 const int64_t* out_end, int accumulate) {
   using Cfg = DmmaGemmCfg<L, KC, WM, WN, NSTAGE>;
   auto kern = leaf_gemm_dmma<L, KC, WM, WN, NSTAGE>;
   SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Cfg::kSmemBytes)));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(A, B, pairs, out_offset, n_out, C);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(A, B, pairs, out_offset, n_out, C, out_end,
+                                                     accumulate);
   SPG_CHECK_LAUNCH(ctx);
 }
 
@@ -265,31 +267,34 @@ int gemm_variant() {
 }
 
 void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const int2* pairs,
-              const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st = nullptr) {
+              const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st = nullptr,
+              const int64_t* out_end = nullptr, int accumulate = 0) {
   if (n_out == 0) return;
   if (!st) st = ctx->stream;
+  if ((out_end || accumulate) && L == 64 && gemm_variant() == 3)
+    fail(SPG_EINVAL, "panel accumulation is not supported by the TMA variant");
   if (L == 64 && gemm_variant() == 3) {
     launch_tma64<3>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 4) {  // 4 warps x 32x32, 2 stages, 3 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
     return;
   }
   if (L == 64 && gemm_variant() == 5) {  // 4 warps x 32x32, 3 stages, 2 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
     return;
   }
   if (L == 64 && gemm_variant() == 6) {  // 4 warps x 32x32, KC=16, 4 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
     return;
   }
   if (L == 64 && gemm_variant() == 8) {  // 4 warps x 32x32, KC=16, 3 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    launch_dmma<64, 16, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
     return;
   }
   if (L == 64 && gemm_variant() == 7) {  // 4 warps x 32x32, KC=16, 6 stages, 2 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C, st);
+    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
     return;
   }
   switch (L) {
@@ -298,25 +303,78 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
         const char* e = std::getenv("SPG_GEMM32");  // developer switch for the L=32 tiling
         return e ? std::atoi(e) : 2;
       }();
-      if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
-      else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
-      else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
-      else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
-      else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
       break;
     }
     case 64:
-      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
       break;
     case 128:
-      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st);
+      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
       break;
     default: {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
-      leaf_gemm_generic<<<grid, 256, 0, st>>>(A, B, pairs, out_offset, n_out, L, C);
+      leaf_gemm_generic<<<grid, 256, 0, st>>>(A, B, pairs, out_offset, n_out, L, C, out_end,
+                                              accumulate);
       SPG_CHECK_LAUNCH(ctx);
     }
   }
+}
+
+// Task list grouped by output block: C block o = Morton key out_keys[o] sums
+// the products pairs[out_offset[o], out_offset[o+1]) (k ascending); with
+// keep_keys the sorted (Morton(i,j) << depth | k) keys stay for B panels.
+struct Plan {
+  int64_t n_surv = 0, n_out = 0;
+  int kbits = 0;
+  DevBuf<uint64_t> keys, out_keys;
+  DevBuf<int64_t> out_offset;
+  DevBuf<int2> pairs;
+};
+
+Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                  bool skip_test, Shard shard, bool keep_keys) {
+  TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard)
+                          : build_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard);
+  Plan pl;
+  pl.n_surv = tl.n_surv;
+  pl.kbits = tl.kbits;
+  const int64_t n_surv = tl.n_surv;
+  if (n_surv) {
+    PhaseTrace tr(ctx, "tasklist.group+pairs");
+    DevBuf<uint8_t> flags(n_surv, ctx);
+    head_flags<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
+                                                              flags.get());
+    SPG_CHECK_LAUNCH(ctx);
+    DevBuf<int64_t> heads(n_surv, ctx);
+    DevBuf<int64_t> n_sel(1, ctx);
+    thrust::counting_iterator<int64_t> it(0);
+    size_t bytes = 0;
+    SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags.get(), heads.get(), n_sel.get(),
+                                        n_surv, ctx->stream));
+    DevBuf<uint8_t> tmp(bytes, ctx);
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flags.get(), heads.get(),
+                                        n_sel.get(), n_surv, ctx->stream));
+    ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
+    pl.n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
+    pl.out_keys = DevBuf<uint64_t>(pl.n_out, ctx);
+    pl.out_offset = DevBuf<int64_t>(pl.n_out + 1, ctx);
+    run_outputs<<<grid_for(pl.n_out + 1, 256), 256, 0, ctx->stream>>>(
+        tl.keys.get(), heads.get(), pl.n_out, n_surv, tl.kbits, pl.out_keys.get(),
+        pl.out_offset.get());
+    SPG_CHECK_LAUNCH(ctx);
+    pl.pairs = DevBuf<int2>(n_surv, ctx);
+    make_pairs<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
+                                                              a->grid_slot, b->grid_slot,
+                                                              pl.pairs.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  if (keep_keys) pl.keys = std::move(tl.keys);
+  return pl;
 }
 
 // The product streamed to host buffers: the GEMM runs in chunks of output
@@ -424,49 +482,19 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   if (a->dimension != b->dimension || a->leaf != b->leaf)
     fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
   if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
+  require_payload(a);
+  require_payload(b);
   if (shard.level < 0 || shard.level > a->depth || shard.index < 0 ||
       shard.index >= (1 << shard.level))
     fail(SPG_EINVAL, "spamm: shard outside the quadtree");
   const int L = a->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard)
-                          : build_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard);
-  const int64_t n_surv = tl.n_surv;
-  // group by output block
-  int64_t n_out = 0;
-  DevBuf<uint64_t> out_keys;
-  DevBuf<int64_t> out_offset;
-  DevBuf<int2> pairs;
-  if (n_surv) {
-    PhaseTrace tr(ctx, "tasklist.group+pairs");
-    DevBuf<uint8_t> flags(n_surv, ctx);
-    head_flags<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
-                                                              flags.get());
-    SPG_CHECK_LAUNCH(ctx);
-    DevBuf<int64_t> heads(n_surv, ctx);
-    DevBuf<int64_t> n_sel(1, ctx);
-    thrust::counting_iterator<int64_t> it(0);
-    size_t bytes = 0;
-    SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags.get(), heads.get(), n_sel.get(),
-                                        n_surv, ctx->stream));
-    DevBuf<uint8_t> tmp(bytes, ctx);
-    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flags.get(), heads.get(),
-                                        n_sel.get(), n_surv, ctx->stream));
-    ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
-    n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
-    out_keys = DevBuf<uint64_t>(n_out, ctx);
-    out_offset = DevBuf<int64_t>(n_out + 1, ctx);
-    run_outputs<<<grid_for(n_out + 1, 256), 256, 0, ctx->stream>>>(
-        tl.keys.get(), heads.get(), n_out, n_surv, tl.kbits, out_keys.get(), out_offset.get());
-    SPG_CHECK_LAUNCH(ctx);
-    pairs = DevBuf<int2>(n_surv, ctx);
-    make_pairs<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
-                                                              a->grid_slot, b->grid_slot,
-                                                              pairs.get());
-    SPG_CHECK_LAUNCH(ctx);
-  }
-  tl.keys.reset();
+  Plan plan = plan_product(ctx, a, b, tau, skip_test, shard, false);
+  const int64_t n_surv = plan.n_surv, n_out = plan.n_out;
+  DevBuf<uint64_t>& out_keys = plan.out_keys;
+  DevBuf<int64_t>& out_offset = plan.out_offset;
+  DevBuf<int2>& pairs = plan.pairs;
   SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
   spg_matrix* c = nullptr;
   if (host) {
@@ -498,6 +526,124 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     SPG_CUDA(cudaEventElapsedTime(&stats->ms_gemm, ctx->ev[3], ctx->ev[4]));
     SPG_CUDA(cudaEventElapsedTime(&stats->ms_finalize, ctx->ev[4], ctx->ev[5]));
     stats->candidates = count_candidates(ctx, a, b, shard);
+  }
+  return c;
+}
+
+namespace {
+// per output block, the pair range whose k lies in [k0, k1) (keys of a block
+// are sorted by k)
+__global__ void panel_ranges(const uint64_t* __restrict__ keys,
+                             const int64_t* __restrict__ out_offset, int64_t n_out, int kbits,
+                             uint32_t k0, uint32_t k1, int64_t* __restrict__ beg,
+                             int64_t* __restrict__ end) {
+  const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o >= n_out) return;
+  const uint64_t kmask = (uint64_t(1) << kbits) - 1;
+  auto lower = [&](int64_t lo, int64_t hi, uint32_t k) {
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((keys[mid] & kmask) < k) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  const int64_t hi = out_offset[o + 1];
+  const int64_t b = lower(out_offset[o], hi, k0);
+  beg[o] = b;
+  end[o] = lower(b, hi, k1);
+}
+
+struct EventSet {
+  cudaEvent_t e[4] = {};
+  EventSet() {
+    for (auto& x : e) SPG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  }
+  ~EventSet() {
+    for (auto& x : e) cudaEventDestroy(x);
+  }
+};
+}  // namespace
+
+// B in host memory: the task list comes from the pyramids
+// alone; C starts at zero and each panel of B's block rows is copied into one
+// of two device buffers on the copy stream while the previous panel's GEMM
+// runs, then every output block continues its accumulator over the products
+// whose k lies in the panel.  Panels ascend in k and the accumulator is
+// stored/reloaded exactly, so each C element sees the same FP64 operation
+// sequence as the resident product: C is bitwise identical.
+spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const spg_bstream* bs,
+                                  double tau, spg_spamm_stats* stats) {
+  const spg_matrix* b = bs->norms;
+  if (a->dimension != b->dimension || a->leaf != b->leaf)
+    fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
+  if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
+  require_payload(a);
+  const int L = a->leaf;
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+  Plan plan = plan_product(ctx, a, b, tau, true, Shard{}, true);
+  const int64_t n_out = plan.n_out;
+  SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+  double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+  DevBuf<double> cguard = DevBuf<double>::adopt(c_payload, n_out * LL, ctx);
+  if (n_out) {
+    SPG_CUDA(cudaMemsetAsync(c_payload, 0, n_out * LL * sizeof(double), ctx->stream));
+    const int64_t cap = bs->max_panel_leaves;
+    DevBuf<double> buf[2] = {DevBuf<double>(cap * LL, ctx), DevBuf<double>(cap * LL, ctx)};
+    DevBuf<int64_t> beg(n_out, ctx), end(n_out, ctx);
+    EventSet ev;  // e[0..1]: panel in buffer i copied; e[2..3]: buffer i free again
+    const int n_panels = static_cast<int>(bs->panel_row.size()) - 1;
+    std::vector<int> live;
+    for (int p = 0; p < n_panels; ++p)
+      if (bs->panel_leaf[p + 1] > bs->panel_leaf[p]) live.push_back(p);
+    auto issue_copy = [&](size_t q) {
+      const int p = live[q], i = static_cast<int>(q & 1);
+      const int64_t lo = bs->panel_leaf[p], cnt = bs->panel_leaf[p + 1] - lo;
+      SPG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev.e[2 + i], 0));
+      SPG_CUDA(cudaMemcpyAsync(buf[i].get(), bs->host_payload + lo * LL,
+                               cnt * LL * sizeof(double), cudaMemcpyHostToDevice,
+                               ctx->copy_stream));
+      SPG_CUDA(cudaEventRecord(ev.e[i], ctx->copy_stream));
+    };
+    // the pool hands out blocks in ctx->stream order: the copy stream starts
+    // after everything queued so far
+    SPG_CUDA(cudaEventRecord(ev.e[2], ctx->stream));
+    SPG_CUDA(cudaEventRecord(ev.e[3], ctx->stream));
+    if (!live.empty()) issue_copy(0);
+    for (size_t q = 0; q < live.size(); ++q) {
+      if (q + 1 < live.size()) issue_copy(q + 1);
+      const int p = live[q], i = static_cast<int>(q & 1);
+      panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
+          plan.keys.get(), plan.out_offset.get(), n_out, plan.kbits,
+          static_cast<uint32_t>(bs->panel_row[p]), static_cast<uint32_t>(bs->panel_row[p + 1]),
+          beg.get(), end.get());
+      SPG_CHECK_LAUNCH(ctx);
+      SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ev.e[i], 0));
+      // pairs hold global sorted leaf indices; the panel buffer starts at leaf lo
+      const double* bbase = buf[i].get() - bs->panel_leaf[p] * LL;
+      run_gemm(ctx, L, a->payload, bbase, plan.pairs.get(), beg.get(), n_out, c_payload,
+               ctx->stream, end.get(), 1);
+      SPG_CUDA(cudaEventRecord(ev.e[2 + i], ctx->stream));
+    }
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+  plan.pairs.reset();
+  plan.out_offset.reset();
+  plan.keys.reset();
+  spg_matrix* c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, plan.out_keys.release(),
+                                            cguard.release());
+  SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+  SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
+  if (stats) {
+    stats->survivors = plan.n_surv;
+    stats->output_blocks = n_out;
+    stats->flops = 2.0 * static_cast<double>(L) * L * L * static_cast<double>(plan.n_surv);
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_tasklist, ctx->ev[2], ctx->ev[3]));
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_gemm, ctx->ev[3], ctx->ev[4]));
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_finalize, ctx->ev[4], ctx->ev[5]));
+    stats->candidates = count_candidates(ctx, a, b);
   }
   return c;
 }

@@ -81,6 +81,7 @@ __global__ void trunc_mark_removed(const int64_t* __restrict__ sorted_index, int
 spg_matrix* truncate_device(spg_context* ctx, const spg_matrix* x, double delta,
                             double* removed_norm, int64_t* removed_count) {
   if (delta < 0.0) fail(SPG_EINVAL, "truncate: delta must be nonnegative");  // :175
+  require_payload(x);
   const int64_t n = x->nnzb;
   const int d = x->depth;
   const double* leaf_level = x->pyramid + level_offset(d);
