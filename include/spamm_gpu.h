@@ -296,6 +296,47 @@ int spg_spamm_with_error_control_streamed(spg_context* ctx, const spg_matrix* a,
                                           int32_t n_taus, spg_matrix** c, double* bounds,
                                           spg_controlled_stats* stats);
 
+/* ---- panel plans: B arriving in block-row panels from any source (host
+ * memory, the GPU owning those rows over NCCL) --------------------------------
+ * B is a norm-only matrix whose leaf slots are sorted by block row
+ * (spg_matrix_from_leaf_norms, spg_bstream_matrix).  A plan holds the task
+ * list of A*B (or of a row shard of it, as spg_spamm_shard) and an all-zero
+ * C; spg_plan_accumulate adds the products whose k lies in block rows
+ * [row_begin, row_end) given B's leaves of those rows (slots
+ * spg_plan_panel_slots(...)) in device memory.  Panels must tile
+ * [0, ceil(n/L)) in ascending order (empty rows may pass d_panel = NULL);
+ * the resulting C is bitwise identical to the resident product.
+ * `stream` (a cudaStream_t, or NULL): the library's work waits for the work
+ * already queued on it, and work queued on it later waits for the library's
+ * use of d_panel, so a caller filling panel buffers on its own stream needs
+ * no host synchronisation. */
+typedef struct spg_plan spg_plan;
+/* a_norms (or NULL): the whole A's norms (spg_matrix_from_leaf_norms) when
+ * `a` holds only the shard's block rows -- the skip tests above the shard
+ * level need the global ancestor norms. */
+int spg_plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* a_norms,
+                    const spg_matrix* b, double tau, int32_t level, int32_t shard,
+                    spg_plan** plan);
+int spg_plan_panel_slots(const spg_plan* plan, int32_t row_begin, int32_t row_end,
+                         int64_t* slot_begin, int64_t* count);
+int spg_plan_accumulate(spg_plan* plan, int32_t row_begin, int32_t row_end,
+                        const double* d_panel, void* stream);
+int spg_plan_finish(spg_plan* plan, spg_matrix** c, spg_spamm_stats* stats);
+void spg_plan_free(spg_plan* plan);
+/* Norm-only matrix from a leaf table (host arrays, sorted by block row; slot
+ * t = leaf t).  nonzero may be NULL (every leaf non-null).  Norms are taken
+ * as given: pass the block_norm values the owning GPU computed (download
+ * norms) for bit-exact bounds. */
+int spg_matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                               int64_t n_leaves, const int32_t* block_rows,
+                               const int32_t* block_cols, const double* norms,
+                               const uint8_t* nonzero, spg_matrix** out);
+/* The non-null leaves of block rows [row_begin, row_end) in (row, column)
+ * order into device memory (at most `capacity` leaves; no host sync -- the
+ * caller knows the count from the leaf table).  `stream` as above. */
+int spg_matrix_gather_rows(const spg_matrix* m, int32_t row_begin, int32_t row_end,
+                           double* d_out, int64_t capacity, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,16 @@ int spg_synth_chain_device(spg_context* ctx, int32_t n, int32_t leaf_size, doubl
 int spg_synth_cluster_device(spg_context* ctx, int32_t n, int32_t leaf_size, double ell,
                              double density, uint64_t site_seed, uint64_t value_seed, double drop,
                              spg_matrix** out);
+/* The same matrices restricted to block rows [row_begin, row_end) (a row
+ * shard; the other rows are null).  Values are those of the full generator
+ * (the cluster scale is the global largest row sum). */
+int spg_synth_chain_device_rows(spg_context* ctx, int32_t n, int32_t leaf_size, double ell,
+                                uint64_t seed, double drop, int32_t row_begin, int32_t row_end,
+                                spg_matrix** out);
+int spg_synth_cluster_device_rows(spg_context* ctx, int32_t n, int32_t leaf_size, double ell,
+                                  double density, uint64_t site_seed, uint64_t value_seed,
+                                  double drop, int32_t row_begin, int32_t row_end,
+                                  spg_matrix** out);
 
 #ifdef __cplusplus
 }

@@ -158,6 +158,20 @@ _SIGNATURES = {
     "spg_spamm_with_error_control_streamed": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp,
                                                         C.c_int32, C.POINTER(_vp), _dp,
                                                         C.POINTER(ControlledStats)]),
+    "spg_plan_create": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32,
+                                  C.POINTER(_vp)]),
+    "spg_plan_panel_slots": (C.c_int, [_vp, C.c_int32, C.c_int32, _i64p, _i64p]),
+    "spg_plan_accumulate": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp]),
+    "spg_plan_finish": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(SpammStats)]),
+    "spg_plan_free": (None, [_vp]),
+    "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
+                                             _dp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
+    "spg_matrix_gather_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64, _vp]),
+    "spg_synth_chain_device_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double, C.c_uint64,
+                                              C.c_double, C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "spg_synth_cluster_device_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double,
+                                                C.c_double, C.c_uint64, C.c_uint64, C.c_double,
+                                                C.c_int32, C.c_int32, C.POINTER(_vp)]),
     "spg_synth_chain_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double,
                                        C.c_int64, _i32p, _i32p, _dp, _i64p]),
     "spg_synth_cluster_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
@@ -627,6 +641,73 @@ class BStream:
             pass
 
 
+class Plan:
+    """Task list of A*B (or a row shard) with B arriving in block-row panels
+    (spg_plan_*): accumulate(r0, r1, panel) for ascending row ranges tiling
+    [0, ceil(n/L)), then finish() -> (C, stats)."""
+
+    def __init__(self, ctx: Context, a: Matrix, b_norms: Matrix, tau: float, level: int = 0,
+                 shard: int = 0, a_norms: Matrix | None = None):
+        self.ctx = ctx
+        self._keep = (a, b_norms, a_norms)
+        self._h = _vp()
+        _check(lib().spg_plan_create(ctx.handle, a.handle,
+                                     a_norms.handle if a_norms is not None else None,
+                                     b_norms.handle, tau, level, shard, C.byref(self._h)))
+
+    def panel_slots(self, r0: int, r1: int):
+        lo, n = C.c_int64(0), C.c_int64(0)
+        _check(lib().spg_plan_panel_slots(self._h, r0, r1, C.byref(lo), C.byref(n)))
+        return lo.value, n.value
+
+    def accumulate(self, r0: int, r1: int, d_panel: int | None, stream: int | None = None):
+        """d_panel: device address of the panel's leaves; stream: cudaStream_t
+        address the panel was produced on (stream-ordered hand-off)."""
+        _check(lib().spg_plan_accumulate(self._h, r0, r1, d_panel or None, stream or None))
+
+    def finish(self):
+        h = _vp()
+        st = SpammStats()
+        _check(lib().spg_plan_finish(self._h, C.byref(h), C.byref(st)))
+        return Matrix(self.ctx, h), st.as_dict()
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().spg_plan_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        if sys is None or sys.is_finalizing():
+            return
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def from_leaf_norms(ctx: Context, dimension: int, leaf_size: int, rows, cols, norms,
+                    nonzero=None) -> Matrix:
+    """Norm-only matrix from a leaf table sorted by block row (slot t = leaf t)."""
+    rows = np.ascontiguousarray(rows, np.int32)
+    cols = np.ascontiguousarray(cols, np.int32)
+    norms = np.ascontiguousarray(norms, np.float64)
+    nz = None if nonzero is None else np.ascontiguousarray(nonzero, np.uint8)
+    h = _vp()
+    _check(lib().spg_matrix_from_leaf_norms(ctx.handle, dimension, leaf_size, rows.shape[0],
+                                            _ptr(rows, C.c_int32), _ptr(cols, C.c_int32),
+                                            _ptr(norms, C.c_double),
+                                            _ptr(nz, C.c_uint8) if nz is not None else None,
+                                            C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def gather_rows(m: Matrix, r0: int, r1: int, d_out: int, capacity: int,
+                stream: int | None = None):
+    """Non-null leaves of block rows [r0, r1) in (row, col) order -> d_out."""
+    _check(lib().spg_matrix_gather_rows(m.handle, r0, r1, d_out or None, capacity,
+                                        stream or None))
+
+
 def sort_by_block_row(rows, cols, payload):
     """Leaves reordered by (block row, block column) for BStream."""
     order = np.lexsort((np.asarray(cols), np.asarray(rows)))
@@ -675,6 +756,23 @@ def synth_cluster_host(n: int, leaf: int, ell: float, density: float, site_seed:
                        value_seed: int, drop: float):
     return _host_synth(lib().spg_synth_cluster_host, n, leaf, ell, density, site_seed,
                        value_seed, drop)
+
+
+def synth_chain_device_rows(ctx: Context, n: int, leaf: int, ell: float, seed: int, drop: float,
+                            row_begin: int, row_end: int) -> Matrix:
+    h = _vp()
+    _check(lib().spg_synth_chain_device_rows(ctx.handle, n, leaf, ell, seed, drop, row_begin,
+                                             row_end, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def synth_cluster_device_rows(ctx: Context, n: int, leaf: int, ell: float, density: float,
+                              site_seed: int, value_seed: int, drop: float, row_begin: int,
+                              row_end: int) -> Matrix:
+    h = _vp()
+    _check(lib().spg_synth_cluster_device_rows(ctx.handle, n, leaf, ell, density, site_seed,
+                                               value_seed, drop, row_begin, row_end, C.byref(h)))
+    return Matrix(ctx, h)
 
 
 def synth_chain_device(ctx: Context, n: int, leaf: int, ell: float, seed: int,

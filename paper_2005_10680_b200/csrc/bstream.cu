@@ -122,7 +122,7 @@ spg_bstream* bstream_create(spg_context* ctx, int32_t dimension, int32_t leaf, i
   }
   int h_bad = 0;
   SPG_CUDA(cudaMemcpy(&h_bad, bad.get(), sizeof(int), cudaMemcpyDeviceToHost));
-  bs->norms = matrix_from_leaf_norms(ctx, dimension, leaf, n, d_rows.get(), d_cols.get(),
+  bs->norms = matrix_from_leaf_norms(ctx, dimension, leaf, n, rows, d_rows.get(), d_cols.get(),
                                      norms.get(), nonzero.get());
   if (h_bad) fail(SPG_EINVAL, "nonzero entry in the padding region of a boundary leaf");
   return bs.release();

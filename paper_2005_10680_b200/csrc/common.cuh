@@ -98,6 +98,9 @@ struct spg_matrix {
   double* pyramid = nullptr;    // sum_l 4^l
   double frob = 0.0;
   bool norms_only = false;      // norms of a host-resident B (spg_bstream): no payload
+  // norms_only: leaves (slots) sorted by block row; slots of block rows
+  // [r0, r1) are [row_slot_begin[r0], row_slot_begin[r1]) (2^depth + 1 entries)
+  std::vector<int64_t> row_slot_begin;
 };
 
 // B kept in host memory and streamed to the GPU in panels of block rows
@@ -263,11 +266,12 @@ int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
 // (bitwise) to spamm_device with B resident
 spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const spg_bstream* b,
                                   double tau, spg_spamm_stats* stats);
-// matrix.cu: norm-only matrix from per-leaf norms (slot = leaf index)
+// matrix.cu: norm-only matrix from per-leaf norms (slot = leaf index);
+// h_rows: the same block rows on the host, sorted ascending
 spg_matrix* matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf,
-                                   int64_t n_leaves, const int32_t* d_rows,
-                                   const int32_t* d_cols, const double* d_norms,
-                                   const uint8_t* d_nonzero);
+                                   int64_t n_leaves, const int32_t* h_rows,
+                                   const int32_t* d_rows, const int32_t* d_cols,
+                                   const double* d_norms, const uint8_t* d_nonzero);
 
 inline void require_payload(const spg_matrix* m) {
   if (m && m->norms_only)

@@ -241,6 +241,34 @@ __global__ void gather_norms(const uint64_t* __restrict__ keys, int64_t n,
   out[t] = level[keys[t]];
 }
 
+// Non-null leaves of block rows [r0, r0 + rows) in (row, col) order: cell
+// (r, c) of the panel in row-major order is flagged when its grid slot is
+// non-null (within a block row, Morton order is column order).
+__global__ void panel_cell_flags(const int32_t* __restrict__ grid_slot, int32_t r0, int32_t rows,
+                                 int32_t nbp, uint8_t* __restrict__ flags) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(rows) * nbp) return;
+  const uint32_t r = static_cast<uint32_t>(r0 + t / nbp), c = static_cast<uint32_t>(t % nbp);
+  flags[t] = grid_slot[morton2(r, c)] >= 0;
+}
+
+__global__ void panel_gather(const double* __restrict__ payload,
+                             const int32_t* __restrict__ grid_slot,
+                             const int64_t* __restrict__ cells, const int64_t* __restrict__ n_sel,
+                             int32_t r0, int32_t nbp, int64_t capacity, int64_t elems,
+                             double* __restrict__ out) {
+  const int64_t n = *n_sel < capacity ? *n_sel : capacity;
+  for (int64_t i = blockIdx.y; i < n; i += gridDim.y) {
+    const int64_t t = cells[i];
+    const uint32_t r = static_cast<uint32_t>(r0 + t / nbp), c = static_cast<uint32_t>(t % nbp);
+    const double* src = payload + static_cast<int64_t>(grid_slot[morton2(r, c)]) * elems;
+    double* dst = out + i * elems;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < elems;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      dst[e] = src[e];
+  }
+}
+
 }  // namespace
 
 void matrix_destroy(spg_matrix* m) {
@@ -288,13 +316,17 @@ spg_matrix* matrix_from_device_leaves(spg_context* ctx, int32_t dimension, int32
 }
 
 spg_matrix* matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf,
-                                   int64_t n_leaves, const int32_t* d_rows,
-                                   const int32_t* d_cols, const double* d_norms,
-                                   const uint8_t* d_nonzero) {
+                                   int64_t n_leaves, const int32_t* h_rows,
+                                   const int32_t* d_rows, const int32_t* d_cols,
+                                   const double* d_norms, const uint8_t* d_nonzero) {
   std::unique_ptr<spg_matrix, void (*)(spg_matrix*)> m(new_matrix(ctx, dimension, leaf),
                                                        matrix_destroy);
   m->norms_only = true;
   m->n_slots = n_leaves;
+  const int32_t nbp = 1 << m->depth;
+  m->row_slot_begin.resize(static_cast<size_t>(nbp) + 1);
+  for (int32_t r = 0; r <= nbp; ++r)
+    m->row_slot_begin[r] = std::lower_bound(h_rows, h_rows + n_leaves, r) - h_rows;
   if (n_leaves > (int64_t(1) << 31) - 1) fail(SPG_EINVAL, "too many leaves");
   const int32_t nb_logical = (dimension + leaf - 1) / leaf;
   DevBuf<int> flags(1, ctx);
@@ -624,6 +656,92 @@ int spg_matrix_free(spg_matrix* m) {
   if (!m) return SPG_OK;
   std::lock_guard<std::mutex> lock(m->ctx->mu);
   matrix_destroy(m);
+  SPG_API_END
+}
+
+
+int spg_matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                               int64_t n_leaves, const int32_t* block_rows,
+                               const int32_t* block_cols, const double* norms,
+                               const uint8_t* nonzero, spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_leaves < 0) fail(SPG_EINVAL, "negative leaf count");
+  if (n_leaves && (!block_rows || !block_cols || !norms)) fail(SPG_EINVAL, "null argument");
+  for (int64_t t = 1; t < n_leaves; ++t)
+    if (block_rows[t] < block_rows[t - 1])
+      fail(SPG_EINVAL, "leaf norms: leaves must be sorted by block row");
+  int32_t padded = 0, depth = 0;
+  check_shape(dimension, leaf_size, &padded, &depth);
+  CtxGuard g(ctx);
+  const int64_t n1 = std::max<int64_t>(n_leaves, 1);
+  DevBuf<int32_t> r(n1, ctx), c(n1, ctx);
+  DevBuf<double> nr(n1, ctx);
+  DevBuf<uint8_t> nz(n1, ctx);
+  if (n_leaves) {
+    SPG_CUDA(cudaMemcpyAsync(r.get(), block_rows, n_leaves * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(c.get(), block_cols, n_leaves * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->stream));
+    SPG_CUDA(cudaMemcpyAsync(nr.get(), norms, n_leaves * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    if (nonzero)
+      SPG_CUDA(cudaMemcpyAsync(nz.get(), nonzero, n_leaves, cudaMemcpyHostToDevice, ctx->stream));
+    else
+      SPG_CUDA(cudaMemsetAsync(nz.get(), 1, n_leaves, ctx->stream));
+  }
+  *out = matrix_from_leaf_norms(ctx, dimension, leaf_size, n_leaves, block_rows, r.get(),
+                                c.get(), nr.get(), nz.get());
+  SPG_API_END
+}
+
+int spg_matrix_gather_rows(const spg_matrix* m, int32_t row_begin, int32_t row_end,
+                           double* d_out, int64_t capacity, void* stream) {
+  SPG_API_BEGIN
+  if (!m) fail(SPG_EINVAL, "null matrix");
+  require_payload(m);
+  const int32_t nbp = 1 << m->depth;
+  if (row_begin < 0 || row_end < row_begin || row_end > nbp)
+    fail(SPG_EINVAL, "gather_rows: bad block row range");
+  if (capacity > 0 && !d_out) fail(SPG_EINVAL, "null output");
+  spg_context* ctx = m->ctx;
+  CtxGuard g(ctx);
+  const int32_t rows = row_end - row_begin;
+  const int64_t cells = static_cast<int64_t>(rows) * nbp;
+  if (cells == 0 || capacity <= 0) return SPG_OK;
+  cudaStream_t foreign = static_cast<cudaStream_t>(stream);
+  cudaEvent_t ev = nullptr;
+  if (foreign && foreign != ctx->stream) {
+    SPG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    SPG_CUDA(cudaEventRecord(ev, foreign));
+    SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
+  }
+  DevBuf<uint8_t> flags(cells, ctx);
+  DevBuf<int64_t> sel(cells, ctx), n_sel(1, ctx);
+  panel_cell_flags<<<grid_for(cells, 256), 256, 0, ctx->stream>>>(m->grid_slot, row_begin, rows,
+                                                                  nbp, flags.get());
+  SPG_CHECK_LAUNCH(ctx);
+  thrust::counting_iterator<int64_t> it(0);
+  size_t bytes = 0;
+  SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags.get(), sel.get(), n_sel.get(),
+                                      cells, ctx->stream));
+  DevBuf<uint8_t> tmp(bytes, ctx);
+  SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flags.get(), sel.get(), n_sel.get(),
+                                      cells, ctx->stream));
+  ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
+  const int64_t elems = static_cast<int64_t>(m->leaf) * m->leaf;
+  const int64_t ylim = std::min<int64_t>(std::min(capacity, cells), 65535);
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>((elems + 255) / 256, 16)),
+            static_cast<unsigned>(ylim));
+  panel_gather<<<grid, 256, 0, ctx->stream>>>(m->payload, m->grid_slot, sel.get(), n_sel.get(),
+                                              row_begin, nbp, capacity, elems, d_out);
+  SPG_CHECK_LAUNCH(ctx);
+  if (ev) {
+    SPG_CUDA(cudaEventRecord(ev, ctx->stream));
+    SPG_CUDA(cudaStreamWaitEvent(foreign, ev, 0));
+    cudaEventDestroy(ev);  // released once the recorded work completes
+  }
   SPG_API_END
 }
 

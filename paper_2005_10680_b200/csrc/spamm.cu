@@ -337,7 +337,9 @@ struct Plan {
 };
 
 Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
-                  bool skip_test, Shard shard, bool keep_keys) {
+                  bool skip_test, Shard shard, bool keep_keys,
+                  const spg_matrix* a_slots = nullptr) {
+  if (!a_slots) a_slots = a;  // a: norms for the skip tests; a_slots: A's payload slots
   TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard)
                           : build_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard);
   Plan pl;
@@ -369,7 +371,7 @@ Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
     SPG_CHECK_LAUNCH(ctx);
     pl.pairs = DevBuf<int2>(n_surv, ctx);
     make_pairs<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
-                                                              a->grid_slot, b->grid_slot,
+                                                              a_slots->grid_slot, b->grid_slot,
                                                               pl.pairs.get());
     SPG_CHECK_LAUNCH(ctx);
   }
@@ -564,36 +566,144 @@ struct EventSet {
   }
 };
 }  // namespace
+}  // namespace spg
 
-// B in host memory: the task list comes from the pyramids
-// alone; C starts at zero and each panel of B's block rows is copied into one
-// of two device buffers on the copy stream while the previous panel's GEMM
-// runs, then every output block continues its accumulator over the products
-// whose k lies in the panel.  Panels ascend in k and the accumulator is
-// stored/reloaded exactly, so each C element sees the same FP64 operation
-// sequence as the resident product: C is bitwise identical.
-spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const spg_bstream* bs,
-                                  double tau, spg_spamm_stats* stats) {
-  const spg_matrix* b = bs->norms;
+// A product whose B arrives in panels of block rows: B from
+// host memory (spg_bstream) or from the GPU that owns those rows (NCCL
+// broadcast, sharded.py).  The task list comes from the norm pyramids alone;
+// C starts at zero and every panel continues each output block's accumulator
+// over the products whose k lies in the panel.  Panels must tile the block
+// rows in ascending order, so each C element sees the same FP64 operation
+// sequence as the resident product and C is bitwise identical to it.
+struct spg_plan {
+  spg_context* ctx = nullptr;
+  const spg_matrix* a = nullptr;
+  const spg_matrix* b = nullptr;  // norm-only, slots sorted by block row
+  spg::Plan pl;
+  spg::DevBuf<double> c;
+  spg::DevBuf<int64_t> beg, end;
+  int32_t next_row = 0;
+  bool finished = false;
+  spg_spamm_stats stats{};
+  cudaEvent_t ev[2] = {};
+  ~spg_plan() {
+    for (auto& x : ev)
+      if (x) cudaEventDestroy(x);
+  }
+};
+
+namespace spg {
+
+// a_norms (optional): the norms of the whole A when `a` holds only the
+// shard's block rows (skip tests above the shard level need the global
+// ancestors); the shard's rows of a_norms must be a's.
+spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                      Shard shard, const spg_matrix* a_norms = nullptr) {
   if (a->dimension != b->dimension || a->leaf != b->leaf)
     fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
+  if (a_norms && (a_norms->dimension != a->dimension || a_norms->leaf != a->leaf))
+    fail(SPG_EINVAL, "plan: A norms do not match A's shape");
   if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
   require_payload(a);
-  const int L = a->leaf;
-  const int64_t LL = static_cast<int64_t>(L) * L;
+  if (!b->norms_only || b->row_slot_begin.empty())
+    fail(SPG_EINVAL, "plan: B must be a norm-only matrix (spg_matrix_from_leaf_norms, "
+                     "spg_bstream)");
+  if (shard.level < 0 || shard.level > a->depth || shard.index < 0 ||
+      shard.index >= (1 << shard.level))
+    fail(SPG_EINVAL, "spamm: shard outside the quadtree");
+  auto plan = std::make_unique<spg_plan>();
+  plan->ctx = ctx;
+  plan->a = a;
+  plan->b = b;
+  for (auto& x : plan->ev) SPG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  const int64_t LL = static_cast<int64_t>(a->leaf) * a->leaf;
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  Plan plan = plan_product(ctx, a, b, tau, true, Shard{}, true);
-  const int64_t n_out = plan.n_out;
+  plan->pl = plan_product(ctx, a_norms ? a_norms : a, b, tau, true, shard, true, a);
   SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
-  double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
-  DevBuf<double> cguard = DevBuf<double>::adopt(c_payload, n_out * LL, ctx);
-  if (n_out) {
-    SPG_CUDA(cudaMemsetAsync(c_payload, 0, n_out * LL * sizeof(double), ctx->stream));
+  const int64_t n_out = plan->pl.n_out;
+  plan->c = DevBuf<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+  if (n_out) SPG_CUDA(cudaMemsetAsync(plan->c.get(), 0, n_out * LL * sizeof(double), ctx->stream));
+  plan->beg = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
+  plan->end = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
+  SPG_CUDA(cudaEventSynchronize(ctx->ev[3]));
+  spg_spamm_stats& st = plan->stats;
+  st.survivors = plan->pl.n_surv;
+  st.output_blocks = n_out;
+  st.flops = 2.0 * static_cast<double>(a->leaf) * a->leaf * a->leaf *
+             static_cast<double>(plan->pl.n_surv);
+  SPG_CUDA(cudaEventElapsedTime(&st.ms_tasklist, ctx->ev[2], ctx->ev[3]));
+  st.candidates = count_candidates(ctx, a, b, shard);
+  return plan.release();
+}
+
+// B slots [row_slot_begin[r0], row_slot_begin[r1]) at d_panel, enqueued on
+// ctx->stream
+void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_panel) {
+  spg_context* ctx = plan->ctx;
+  const spg_matrix* b = plan->b;
+  const int32_t nbp = 1 << b->depth;
+  if (plan->finished) fail(SPG_EINVAL, "plan: already finished");
+  if (r0 != plan->next_row)
+    fail(SPG_EINVAL, "plan: panels must tile the block rows in ascending order (expected row " +
+                         std::to_string(plan->next_row) + ")");
+  if (r1 <= r0 || r1 > nbp) fail(SPG_EINVAL, "plan: bad panel row range");
+  const int64_t lo = b->row_slot_begin[r0], cnt = b->row_slot_begin[r1] - lo;
+  if (cnt > 0 && !d_panel) fail(SPG_EINVAL, "plan: panel holds leaves but no buffer was given");
+  plan->next_row = r1;
+  const int64_t n_out = plan->pl.n_out;
+  if (n_out == 0 || cnt == 0) return;
+  const int L = b->leaf;
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
+      plan->pl.keys.get(), plan->pl.out_offset.get(), n_out, plan->pl.kbits,
+      static_cast<uint32_t>(r0), static_cast<uint32_t>(r1), plan->beg.get(), plan->end.get());
+  SPG_CHECK_LAUNCH(ctx);
+  // pairs hold B slots; the panel buffer starts at slot lo
+  run_gemm(ctx, L, plan->a->payload, d_panel - lo * LL, plan->pl.pairs.get(), plan->beg.get(),
+           n_out, plan->c.get(), ctx->stream, plan->end.get(), 1);
+}
+
+spg_matrix* plan_finish(spg_plan* plan) {
+  spg_context* ctx = plan->ctx;
+  const spg_matrix* a = plan->a;
+  const int32_t nb_logical = (a->dimension + a->leaf - 1) / a->leaf;
+  if (plan->finished) fail(SPG_EINVAL, "plan: already finished");
+  if (plan->next_row < nb_logical)
+    fail(SPG_EINVAL, "plan: panels cover block rows [0, " + std::to_string(plan->next_row) +
+                         ") only");
+  plan->finished = true;
+  SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+  plan->pl.pairs.reset();
+  plan->pl.out_offset.reset();
+  plan->pl.keys.reset();
+  plan->beg.reset();
+  plan->end.reset();
+  spg_matrix* c = matrix_from_morton_blocks(ctx, a->dimension, a->leaf, plan->pl.n_out,
+                                            plan->pl.out_keys.release(), plan->c.release());
+  SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+  SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
+  SPG_CUDA(cudaEventElapsedTime(&plan->stats.ms_finalize, ctx->ev[4], ctx->ev[5]));
+  return c;
+}
+
+// B in host memory (spg_bstream): panels copied into two device buffers on
+// the copy stream, panel q+1 in flight while panel q's GEMM runs.
+spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const spg_bstream* bs,
+                                  double tau, spg_spamm_stats* stats) {
+  std::unique_ptr<spg_plan> plan(plan_create(ctx, a, bs->norms, tau, Shard{}));
+  const int64_t LL = static_cast<int64_t>(a->leaf) * a->leaf;
+  SPG_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
+  const int n_panels = static_cast<int>(bs->panel_row.size()) - 1;
+  if (plan->pl.n_out == 0) {
+    plan->next_row = bs->panel_row.back();
+  } else {
     const int64_t cap = bs->max_panel_leaves;
     DevBuf<double> buf[2] = {DevBuf<double>(cap * LL, ctx), DevBuf<double>(cap * LL, ctx)};
-    DevBuf<int64_t> beg(n_out, ctx), end(n_out, ctx);
     EventSet ev;  // e[0..1]: panel in buffer i copied; e[2..3]: buffer i free again
-    const int n_panels = static_cast<int>(bs->panel_row.size()) - 1;
+    // the pool hands out blocks in ctx->stream order: the copy stream starts
+    // after everything queued so far
+    SPG_CUDA(cudaEventRecord(ev.e[2], ctx->stream));
+    SPG_CUDA(cudaEventRecord(ev.e[3], ctx->stream));
     std::vector<int> live;
     for (int p = 0; p < n_panels; ++p)
       if (bs->panel_leaf[p + 1] > bs->panel_leaf[p]) live.push_back(p);
@@ -606,44 +716,28 @@ spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const s
                                ctx->copy_stream));
       SPG_CUDA(cudaEventRecord(ev.e[i], ctx->copy_stream));
     };
-    // the pool hands out blocks in ctx->stream order: the copy stream starts
-    // after everything queued so far
-    SPG_CUDA(cudaEventRecord(ev.e[2], ctx->stream));
-    SPG_CUDA(cudaEventRecord(ev.e[3], ctx->stream));
     if (!live.empty()) issue_copy(0);
-    for (size_t q = 0; q < live.size(); ++q) {
+    size_t q = 0;
+    for (int p = 0; p < n_panels; ++p) {
+      const bool has = q < live.size() && live[q] == p;
+      if (!has) {  // no leaves in these rows
+        plan_accumulate(plan.get(), bs->panel_row[p], bs->panel_row[p + 1], nullptr);
+        continue;
+      }
       if (q + 1 < live.size()) issue_copy(q + 1);
-      const int p = live[q], i = static_cast<int>(q & 1);
-      panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
-          plan.keys.get(), plan.out_offset.get(), n_out, plan.kbits,
-          static_cast<uint32_t>(bs->panel_row[p]), static_cast<uint32_t>(bs->panel_row[p + 1]),
-          beg.get(), end.get());
-      SPG_CHECK_LAUNCH(ctx);
+      const int i = static_cast<int>(q & 1);
       SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ev.e[i], 0));
-      // pairs hold global sorted leaf indices; the panel buffer starts at leaf lo
-      const double* bbase = buf[i].get() - bs->panel_leaf[p] * LL;
-      run_gemm(ctx, L, a->payload, bbase, plan.pairs.get(), beg.get(), n_out, c_payload,
-               ctx->stream, end.get(), 1);
+      plan_accumulate(plan.get(), bs->panel_row[p], bs->panel_row[p + 1], buf[i].get());
       SPG_CUDA(cudaEventRecord(ev.e[2 + i], ctx->stream));
+      ++q;
     }
     SPG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
-  SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
-  plan.pairs.reset();
-  plan.out_offset.reset();
-  plan.keys.reset();
-  spg_matrix* c = matrix_from_morton_blocks(ctx, a->dimension, L, n_out, plan.out_keys.release(),
-                                            cguard.release());
-  SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
-  SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
+  SPG_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
+  spg_matrix* c = plan_finish(plan.get());
   if (stats) {
-    stats->survivors = plan.n_surv;
-    stats->output_blocks = n_out;
-    stats->flops = 2.0 * static_cast<double>(L) * L * L * static_cast<double>(plan.n_surv);
-    SPG_CUDA(cudaEventElapsedTime(&stats->ms_tasklist, ctx->ev[2], ctx->ev[3]));
-    SPG_CUDA(cudaEventElapsedTime(&stats->ms_gemm, ctx->ev[3], ctx->ev[4]));
-    SPG_CUDA(cudaEventElapsedTime(&stats->ms_finalize, ctx->ev[4], ctx->ev[5]));
-    stats->candidates = count_candidates(ctx, a, b);
+    *stats = plan->stats;
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_gemm, ctx->ev[6], ctx->ev[7]));
   }
   return c;
 }
@@ -857,6 +951,86 @@ int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
     }
   }
   SPG_API_END
+}
+
+// ---- panel plans (B arriving in block-row panels) -------------------------
+namespace {
+// make ctx->stream wait for `foreign` (the caller's stream) and, after the
+// enqueued work, `foreign` wait for ctx->stream: stream-ordered hand-off
+struct ForeignOrder {
+  spg_context* ctx;
+  cudaStream_t foreign;
+  cudaEvent_t ev;
+  ForeignOrder(spg_context* c, void* s, cudaEvent_t e)
+      : ctx(c), foreign(static_cast<cudaStream_t>(s)), ev(e) {
+    if (foreign && foreign != ctx->stream) {
+      SPG_CUDA(cudaEventRecord(ev, foreign));
+      SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
+    }
+  }
+  void done() {
+    if (foreign && foreign != ctx->stream) {
+      SPG_CUDA(cudaEventRecord(ev, ctx->stream));
+      SPG_CUDA(cudaStreamWaitEvent(foreign, ev, 0));
+    }
+  }
+};
+}  // namespace
+
+int spg_plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* a_norms,
+                    const spg_matrix* b, double tau, int32_t level, int32_t shard,
+                    spg_plan** plan) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !plan) fail(SPG_EINVAL, "null argument");
+  *plan = nullptr;
+  if (a->ctx != ctx || b->ctx != ctx || (a_norms && a_norms->ctx != ctx))
+    fail(SPG_EINVAL, "operands belong to another context");
+  CtxGuard g(ctx);
+  *plan = plan_create(ctx, a, b, tau, Shard{level, shard}, a_norms);
+  SPG_API_END
+}
+
+int spg_plan_panel_slots(const spg_plan* plan, int32_t row_begin, int32_t row_end,
+                         int64_t* slot_begin, int64_t* count) {
+  SPG_API_BEGIN
+  if (!plan) fail(SPG_EINVAL, "null argument");
+  const auto& rs = plan->b->row_slot_begin;
+  const int32_t nbp = static_cast<int32_t>(rs.size()) - 1;
+  if (row_begin < 0 || row_end < row_begin || row_end > nbp)
+    fail(SPG_EINVAL, "plan: bad panel row range");
+  if (slot_begin) *slot_begin = rs[row_begin];
+  if (count) *count = rs[row_end] - rs[row_begin];
+  SPG_API_END
+}
+
+int spg_plan_accumulate(spg_plan* plan, int32_t row_begin, int32_t row_end,
+                        const double* d_panel, void* stream) {
+  SPG_API_BEGIN
+  if (!plan) fail(SPG_EINVAL, "null argument");
+  CtxGuard g(plan->ctx);
+  ForeignOrder fo(plan->ctx, stream, plan->ev[0]);
+  plan_accumulate(plan, row_begin, row_end, d_panel);
+  fo.done();
+  SPG_API_END
+}
+
+int spg_plan_finish(spg_plan* plan, spg_matrix** c, spg_spamm_stats* stats) {
+  SPG_API_BEGIN
+  if (!plan || !c) fail(SPG_EINVAL, "null argument");
+  *c = nullptr;
+  CtxGuard g(plan->ctx);
+  *c = plan_finish(plan);
+  if (stats) *stats = plan->stats;
+  SPG_API_END
+}
+
+void spg_plan_free(spg_plan* plan) {
+  if (!plan) return;
+  try {
+    CtxGuard g(plan->ctx);
+    delete plan;
+  } catch (...) {
+  }
 }
 
 }  // extern "C"

@@ -94,15 +94,20 @@ __host__ __device__ inline double site_distance(const double* p, const double* q
 #endif
 }
 
-// Enumerate leaf blocks of the logical grid in Morton order.
-std::vector<uint64_t> morton_blocks(int32_t nb_logical, int depth) {
+// Enumerate leaf blocks of the logical grid in Morton order (block rows
+// [row_begin, row_end) only, when given).
+std::vector<uint64_t> morton_blocks(int32_t nb_logical, int depth, int32_t row_begin = 0,
+                                    int32_t row_end = -1) {
+  if (row_end < 0) row_end = nb_logical;
   std::vector<uint64_t> keys;
-  keys.reserve(static_cast<size_t>(nb_logical) * nb_logical);
+  keys.reserve(static_cast<size_t>(std::max(row_end - row_begin, 0)) * nb_logical);
   const uint64_t total = uint64_t(1) << (2 * depth);
-  for (uint64_t key = 0; key < total; ++key)
-    if (morton_row(key) < static_cast<uint32_t>(nb_logical) &&
+  for (uint64_t key = 0; key < total; ++key) {
+    const uint32_t r = morton_row(key);
+    if (r >= static_cast<uint32_t>(row_begin) && r < static_cast<uint32_t>(row_end) &&
         morton_col(key) < static_cast<uint32_t>(nb_logical))
       keys.push_back(key);
+  }
   return keys;
 }
 
@@ -300,16 +305,25 @@ int spg_synth_cluster_host(int32_t n, int32_t L, double ell, double density, uin
 
 int spg_synth_chain_device(spg_context* ctx, int32_t n, int32_t L, double ell, uint64_t seed,
                            double drop, spg_matrix** out) {
+  return spg_synth_chain_device_rows(ctx, n, L, ell, seed, drop, 0, (n + L - 1) / std::max(L, 1),
+                                     out);
+}
+
+int spg_synth_chain_device_rows(spg_context* ctx, int32_t n, int32_t L, double ell, uint64_t seed,
+                                double drop, int32_t row_begin, int32_t row_end,
+                                spg_matrix** out) {
   SPG_API_BEGIN
   if (!ctx || !out) fail(SPG_EINVAL, "null argument");
   *out = nullptr;
   if (!(ell > 0.0)) fail(SPG_EINVAL, "ell must be positive");
   int32_t padded, depth;
   check_shape(n, L, &padded, &depth);
-  CtxGuard g(ctx);
   const int32_t nb = (n + L - 1) / L;
+  if (row_begin < 0 || row_end < row_begin || row_end > nb)
+    fail(SPG_EINVAL, "synth: bad block row range");
+  CtxGuard g(ctx);
   std::vector<uint64_t> hkeys;
-  for (uint64_t key : morton_blocks(nb, depth)) {
+  for (uint64_t key : morton_blocks(nb, depth, row_begin, row_end)) {
     const int64_t gap =
         std::max<int64_t>(0, std::llabs(int64_t(morton_row(key)) - morton_col(key)) * L - (L - 1));
     if (drop <= 0.0 || std::exp(-(static_cast<double>(gap) / ell)) >= drop * 0.5)
@@ -333,6 +347,14 @@ int spg_synth_chain_device(spg_context* ctx, int32_t n, int32_t L, double ell, u
 int spg_synth_cluster_device(spg_context* ctx, int32_t n, int32_t L, double ell, double density,
                              uint64_t site_seed, uint64_t value_seed, double drop,
                              spg_matrix** out) {
+  return spg_synth_cluster_device_rows(ctx, n, L, ell, density, site_seed, value_seed, drop, 0,
+                                       (n + L - 1) / std::max(L, 1), out);
+}
+
+int spg_synth_cluster_device_rows(spg_context* ctx, int32_t n, int32_t L, double ell,
+                                  double density, uint64_t site_seed, uint64_t value_seed,
+                                  double drop, int32_t row_begin, int32_t row_end,
+                                  spg_matrix** out) {
   SPG_API_BEGIN
   if (!ctx || !out) fail(SPG_EINVAL, "null argument");
   *out = nullptr;
@@ -340,6 +362,8 @@ int spg_synth_cluster_device(spg_context* ctx, int32_t n, int32_t L, double ell,
   if (!(ell > 0.0) || !(density > 0.0)) fail(SPG_EINVAL, "ell and density must be positive");
   int32_t padded, depth;
   check_shape(n, L, &padded, &depth);
+  if (row_begin < 0 || row_end < row_begin || row_end > (n + L - 1) / L)
+    fail(SPG_EINVAL, "synth: bad block row range");
   CtxGuard g(ctx);
   const std::vector<double> sites = cluster_sites(n / 4, density, site_seed, nullptr);
   DevBuf<double> dsites(sites.size(), ctx);
@@ -353,7 +377,7 @@ int spg_synth_cluster_device(spg_context* ctx, int32_t n, int32_t L, double ell,
   max_kernel<<<1, 256, 0, ctx->stream>>>(rowsum.get(), n, scale.get());
   SPG_CHECK_LAUNCH(ctx);
   const int32_t nb = (n + L - 1) / L;
-  const std::vector<uint64_t> hkeys = morton_blocks(nb, depth);
+  const std::vector<uint64_t> hkeys = morton_blocks(nb, depth, row_begin, row_end);
   const int64_t nblk = static_cast<int64_t>(hkeys.size());
   const int64_t LL = static_cast<int64_t>(L) * L;
   DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx);

@@ -29,3 +29,144 @@ def controlled_product_shard(ctx, A, B, delta: float, taus, level: int, shard: i
     C, st = nat.spamm_shard(ctx, A, B, tau, level, shard)
     return C, {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
                "spamm": st}, bounds
+
+
+# --------------------------------------------------------------------------
+# Operands distributed by block row: rank g holds
+# only its shard's block rows of A and of B.  Every rank all-gathers the two
+# leaf-norm tables (block_norm values computed by the owning GPU, so the
+# global norm pyramids are bit-exact), runs the sweep on its shard, and then
+# builds its rows of C~ from B panels broadcast by their owners -- ascending
+# block rows, double-buffered against the panel GEMMs (spg_plan_*).  C~ is
+# bitwise the single-GPU product's rows.
+
+def leaf_table(M):
+    """(rows, cols, norms) of M's non-null leaves, sorted by (row, col)."""
+    import numpy as np
+    r, c, _, nrm = M.download(payload=False)
+    order = np.lexsort((c, r))
+    return r[order], c[order], nrm[order]
+
+
+def merge_tables(tables):
+    """Union of per-rank leaf tables (disjoint block rows) in (row, col) order."""
+    import numpy as np
+    r = np.concatenate([t[0] for t in tables]).astype(np.int32)
+    c = np.concatenate([t[1] for t in tables]).astype(np.int32)
+    n = np.concatenate([t[2] for t in tables]).astype(np.float64)
+    order = np.lexsort((c, r))
+    r, c, n = r[order], c[order], n[order]
+    if len(r) > 1:
+        dup = (r[1:] == r[:-1]) & (c[1:] == c[:-1])
+        if dup.any():
+            raise ValueError("leaf tables overlap: shards must own disjoint block rows")
+    return r, c, n
+
+
+def panel_schedule(n: int, leaf: int, level: int, panel_rows: int):
+    """[(r0, r1, owner)] tiling block rows [0, ceil(n/L)) in ascending order;
+    a panel never crosses a shard boundary (owner = shard of its rows)."""
+    if panel_rows < 1:
+        raise ValueError("panel_rows must be positive")
+    nb = -(-n // leaf)
+    depth = 0
+    while (leaf << depth) < n:
+        depth += 1
+    rows_per = (1 << depth) >> level
+    out = []
+    for g in range(1 << level):
+        lo, hi = g * rows_per, min((g + 1) * rows_per, nb)
+        for r in range(lo, hi, panel_rows):
+            out.append((r, min(r + panel_rows, hi), g))
+    return out
+
+
+def run_panels(ctx, plan, schedule, fetch, leaf: int):
+    """Feed `plan` the B panels of `schedule`, two in flight: fetch(r0, r1,
+    owner, buf, count, stream) fills buf (count leaves) on `stream`; the
+    panel GEMM waits for that stream, and the buffer's next fill waits for
+    the GEMM (stream-ordered, no host synchronisation)."""
+    import torch
+    LL = leaf * leaf
+    counts = [plan.panel_slots(r0, r1)[1] for r0, r1, _ in schedule]
+    cap = max(counts, default=0)
+    dev = torch.device("cuda", ctx.device)
+    bufs = [torch.empty(max(cap * LL, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
+    live = [q for q, cnt in enumerate(counts) if cnt > 0]
+    slot = {q: i % 2 for i, q in enumerate(live)}
+
+    def issue(q):
+        r0, r1, owner = schedule[q]
+        i = slot[q]
+        with torch.cuda.stream(streams[i]):
+            fetch(r0, r1, owner, bufs[i], counts[q], streams[i])
+
+    nxt = iter(live)
+    pending = next(nxt, None)
+    if pending is not None:
+        issue(pending)
+        pending = next(nxt, None)
+    for q, (r0, r1, owner) in enumerate(schedule):
+        if counts[q] == 0:
+            plan.accumulate(r0, r1, None)
+            continue
+        if pending is not None:  # panel after this one goes in flight first
+            issue(pending)
+            pending = next(nxt, None)
+        i = slot[q]
+        plan.accumulate(r0, r1, bufs[i].data_ptr(), streams[i].cuda_stream)
+    ctx.synchronize()
+    return sum(counts) * LL * 8
+
+
+def torch_fetch(comm_backend: str, rank: int, B_local, leaf: int):
+    """fetch() for run_panels over torch.distributed: the owner gathers its
+    rows of B into the buffer, then a broadcast from the owner (NCCL on the
+    buffer's stream; gloo through host memory)."""
+    import torch
+    import torch.distributed as dist
+    LL = leaf * leaf
+
+    def fetch(r0, r1, owner, buf, count, stream):
+        view = buf[: count * LL]
+        if owner == rank:
+            nat.gather_rows(B_local, r0, r1, buf.data_ptr(), count, stream.cuda_stream)
+        if comm_backend == "nccl":
+            dist.broadcast(view, src=owner)
+        else:
+            stream.synchronize()
+            host = view.cpu() if owner == rank else torch.empty(count * LL, dtype=torch.float64)
+            dist.broadcast(host, src=owner)
+            if owner != rank:
+                view.copy_(host)
+            stream.synchronize()
+    return fetch
+
+
+def controlled_product_distributed(ctx, A_local, B_local, delta: float, taus, level: int,
+                                   rank: int, allgather, fetch, panel_rows: int = 8):
+    """Rank `rank` of 2^level: C~ rows of its shard for A*B with A and B
+    distributed by block row.  allgather(list_of_arrays) -> per-rank lists
+    (variable lengths); fetch as in run_panels."""
+    import numpy as np
+    if not (delta > 0.0):
+        raise ValueError("spamm_with_error_control: delta must be positive")
+    taus = np.ascontiguousarray(taus, np.float64)
+    nat.tolerance_grid_check(taus)
+    n, L = A_local.dimension, A_local.leaf_size
+    ta = merge_tables(allgather(list(leaf_table(A_local))))
+    tb = merge_tables(allgather(list(leaf_table(B_local))))
+    A_norms = nat.from_leaf_norms(ctx, n, L, *ta)
+    B_norms = nat.from_leaf_norms(ctx, n, L, *tb)
+    partial = nat.cse_shard(ctx, A_norms, B_norms, taus, level, rank)
+    parts = np.stack([p[0] for p in allgather([partial])])
+    bounds = nat.cse_finish(level, nat.top_norms(A_norms, level), nat.top_norms(B_norms, level),
+                            parts)
+    tau, k = nat.select_tolerance(bounds, taus, delta)
+    plan = nat.Plan(ctx, A_local, B_norms, tau, level, rank, a_norms=A_norms)
+    moved = run_panels(ctx, plan, panel_schedule(n, L, level, panel_rows), fetch, L)
+    C, st = plan.finish()
+    plan.free()
+    return C, {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
+               "spamm": st, "panel_bytes": moved}, bounds
