@@ -58,6 +58,10 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2"])
+    p.add_argument("--operands", default="replicated", choices=["replicated", "distributed"],
+                   help="distributed: each rank holds only its block rows of A and B; B panels "
+                        "are broadcast by their owners (SURVEY 8e, configs 4/5)")
+    p.add_argument("--panel-rows", type=int, default=32)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=4,
@@ -222,20 +226,50 @@ def run_ours(args, dist):
     from paper_2005_10680_b200 import _native as nat
     from paper_2005_10680_b200.inputs import CONFIGS, log_grid
 
-    from paper_2005_10680_b200.sharded import controlled_product_shard
+    from paper_2005_10680_b200.sharded import (DistributedOperands, controlled_product_shard,
+                                               torch_fetch)
 
     w = CONFIGS[args.workload]
     torch.cuda.set_device(dist.device)
     ctx = nat.Context(dist.device)
     stream = torch.cuda.ExternalStream(ctx.stream)
-    A = make_matrix(nat, ctx, w)
     taus = log_grid(w.n_taus)
     # N = 2^s ranks: output block-row shards + NCCL all-gather of the level-s
     # CSE vectors; other N: independent replicas
     level = dist.world.bit_length() - 1
-    sharded = dist.world > 1 and 2 ** level == dist.world
+    distributed = args.operands == "distributed"
+    if distributed and 2 ** level != dist.world:
+        raise SystemExit("--operands distributed needs a power-of-two GPU count")
+    sharded = dist.world > 1 and 2 ** level == dist.world and not distributed
+    split = sharded or distributed  # per-rank stats summed over ranks
+    if distributed:
+        nb = -(-w.n // w.leaf)
+        rows_per = (1 << max(0, (nb - 1).bit_length())) >> level
+        lo, hi = min(dist.rank * rows_per, nb), min((dist.rank + 1) * rows_per, nb)
+        if w.kind == "cluster":
+            A = nat.synth_cluster_device_rows(ctx, w.n, w.leaf, w.ell, w.density, w.site_seed,
+                                              w.value_seed, w.drop, lo, hi)
+        else:
+            A = nat.synth_chain_device_rows(ctx, w.n, w.leaf, w.ell, w.value_seed, w.drop, lo, hi)
+
+        def allgather(arrays):
+            if dist.world == 1:
+                return [arrays]
+            out = [None] * dist.world
+            dist.pg.all_gather_object(out, arrays)
+            return out
+        ops = DistributedOperands(ctx, A, A, level, dist.rank, allgather)
+        fetch = torch_fetch(dist.backend or "none", dist.rank, A, w.leaf)
+    else:
+        A = make_matrix(nat, ctx, w)
 
     def step():
+        if distributed:
+            t0 = time.perf_counter()
+            C, st, b = ops.controlled_product(w.delta, taus, fetch, args.panel_rows)
+            st["ms_cse"] = None
+            st["ms_step_host"] = 1e3 * (time.perf_counter() - t0)
+            return C, st, b
         if not sharded:
             return nat.spamm_with_error_control(ctx, A, A, w.delta, taus)
         t0 = time.perf_counter()
@@ -275,33 +309,42 @@ def run_ours(args, dist):
     st = stats[-1]
     sp = st["spamm"]
     gemm_ms = sum(s["spamm"]["ms_gemm"] for s in stats) / len(stats)
-    if sharded:  # sweep = step minus the product phases (host-measured)
+    if split:  # sweep = step minus the product phases (host-measured)
         cse_ms = sum(s["ms_step_host"] - s["spamm"]["ms_tasklist"] - s["spamm"]["ms_gemm"] -
                      s["spamm"]["ms_finalize"] for s in stats) / len(stats)
         cse_ms = dist.max(cse_ms)
     else:
         cse_ms = sum(s["ms_cse"] for s in stats) / len(stats)
-    achieved = sp["flops"] / (gemm_ms / 1e3) / 1e12
+    achieved = sp["flops"] / (max(gemm_ms, 1e-6) / 1e3) / 1e12
+    A_bytes = float(A.nnz_blocks) * w.leaf * w.leaf * 8
     hbm, hbm_src = hbm_peak()
-    cand = dist.sum(float(sp["candidates"])) if sharded else float(sp["candidates"])
-    surv = dist.sum(float(sp["survivors"])) if sharded else float(sp["survivors"])
+    cand = dist.sum(float(sp["candidates"])) if split else float(sp["candidates"])
+    surv = dist.sum(float(sp["survivors"])) if split else float(sp["survivors"])
     sweep_bytes = 12.0 * cand
     sweep_gbs = sweep_bytes / (cse_ms / 1e3) / 1e9
 
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3),
-        "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if split else "weak", "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic: seeded 3-D cluster decay matrix (DESIGN.md Inputs), generated on device",
+        "data": (f"synthetic: seeded {'3-D cluster' if w.kind == 'cluster' else '1-D chain'} "
+                 f"decay matrix (DESIGN.md Inputs), generated on device"),
         "config": {"workload": w.name, "n": w.n, "leaf": w.leaf, "ell": w.ell,
                    "density": w.density, "delta": w.delta, "n_taus": w.n_taus,
                    "tau_grid": "log-spaced [1e-12, 1e-2]", "drop": w.drop,
-                   "parallelism": (f"row-shards x{dist.world} (level {level}), "
+                   "parallelism": (f"distributed operands x{dist.world} (level {level}): "
+                                   f"block-row shards of A and B, all-gathered norm tables, "
+                                   f"B panels of {args.panel_rows} block rows broadcast by "
+                                   f"their owners ({dist.backend or 'local'})"
+                                   if distributed else
+                                   f"row-shards x{dist.world} (level {level}), "
                                    f"{dist.backend} all-gather of level-{level} CSE vectors"
                                    if sharded else
                                    f"replicas x{dist.world}" if dist.world > 1 else "single"),
-                   "l2": "no flush: each step streams 8.6 GB of leaves (>> 126 MB L2)"},
+                   "l2": (f"no flush: each step streams {A_bytes / 1e9:.1f} GB of leaves "
+                          f"(>> 126 MB L2)" if A_bytes > 1e9 else
+                          f"no flush: {A_bytes / 1e6:.0f} MB of leaves")},
         "pct_peak": round(100.0 * value / DMMA_PEAK_TFLOPS, 2),
         "sweep_ms": round(cse_ms, 4),
         "tau": st["tau"], "tau_index": st["tau_index"], "bound": st["bound"],
@@ -314,7 +357,8 @@ def run_ours(args, dist):
         "roofline": {"kernel": "leaf_gemm_dmma<64>", "bound": "tensor",
                      "achieved": round(achieved, 3), "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / DMMA_PEAK_TFLOPS, 4),
-                     "traffic": traffic_from_profile(), "peak_source": PEAK_SOURCE,
+                     "traffic": traffic_from_profile() if w.name.startswith("cfg2") else None,
+                     "peak_source": PEAK_SOURCE,
                      "algorithmic": "2*L^3*|S(tau)| flops per launch (one launch per step)"},
         "sweep_roofline": {"kernel": "cse (tile + reduce)", "bound": "hbm",
                            "achieved": round(sweep_gbs, 2), "peak": hbm, "unit": "GB/s",
@@ -324,15 +368,17 @@ def run_ours(args, dist):
     }
     if clk:
         out["clocks"] = clk
-    if not sharded:  # SURVEY 8a parity audit: how close the decisions are to ties
+    if distributed:
+        out["panel_bytes_per_step"] = int(st["panel_bytes"])
+    if not split:  # SURVEY 8a parity audit: how close the decisions are to ties
         ties, cands = nat.parity_audit(ctx, A, A, st["tau"], 4)
         out["parity_audit"] = {"near_ties_4ulp": ties, "candidates": cands,
                                "bound_margin": (w.delta - st["bound"]) / w.delta}
 
     host = None
-    if not args.no_e2e and not sharded:
+    if not args.no_e2e and not split:
         out["e2e"], host = run_e2e(args, nat, ctx, stream, A, w, taus)
-    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline and not distributed:
         out["cpu_baseline"] = run_cpu_baseline(args, nat, A, w, taus, st["tau"], host)
     return out
 

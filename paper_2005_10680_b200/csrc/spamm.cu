@@ -586,9 +586,13 @@ struct spg_plan {
   bool finished = false;
   spg_spamm_stats stats{};
   cudaEvent_t ev[2] = {};
+  cudaEvent_t t_first = nullptr, t_last = nullptr;  // GEMM phase: first panel .. finish
+  bool started = false;
   ~spg_plan() {
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
+    if (t_first) cudaEventDestroy(t_first);
+    if (t_last) cudaEventDestroy(t_last);
   }
 };
 
@@ -616,6 +620,8 @@ spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b
   plan->a = a;
   plan->b = b;
   for (auto& x : plan->ev) SPG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  SPG_CUDA(cudaEventCreate(&plan->t_first));
+  SPG_CUDA(cudaEventCreate(&plan->t_last));
   const int64_t LL = static_cast<int64_t>(a->leaf) * a->leaf;
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   plan->pl = plan_product(ctx, a_norms ? a_norms : a, b, tau, true, shard, true, a);
@@ -652,6 +658,10 @@ void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_pan
   plan->next_row = r1;
   const int64_t n_out = plan->pl.n_out;
   if (n_out == 0 || cnt == 0) return;
+  if (!plan->started) {
+    SPG_CUDA(cudaEventRecord(plan->t_first, ctx->stream));
+    plan->started = true;
+  }
   const int L = b->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
   panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
@@ -673,6 +683,7 @@ spg_matrix* plan_finish(spg_plan* plan) {
                          ") only");
   plan->finished = true;
   SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+  SPG_CUDA(cudaEventRecord(plan->t_last, ctx->stream));
   plan->pl.pairs.reset();
   plan->pl.out_offset.reset();
   plan->pl.keys.reset();
@@ -683,6 +694,8 @@ spg_matrix* plan_finish(spg_plan* plan) {
   SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
   SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   SPG_CUDA(cudaEventElapsedTime(&plan->stats.ms_finalize, ctx->ev[4], ctx->ev[5]));
+  if (plan->started)
+    SPG_CUDA(cudaEventElapsedTime(&plan->stats.ms_gemm, plan->t_first, plan->t_last));
   return c;
 }
 

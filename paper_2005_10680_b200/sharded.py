@@ -132,6 +132,8 @@ def torch_fetch(comm_backend: str, rank: int, B_local, leaf: int):
         view = buf[: count * LL]
         if owner == rank:
             nat.gather_rows(B_local, r0, r1, buf.data_ptr(), count, stream.cuda_stream)
+        if comm_backend not in ("nccl", "gloo"):  # one rank: the panel is local
+            return
         if comm_backend == "nccl":
             dist.broadcast(view, src=owner)
         else:
@@ -144,29 +146,51 @@ def torch_fetch(comm_backend: str, rank: int, B_local, leaf: int):
     return fetch
 
 
+class DistributedOperands:
+    """A and B distributed by block row: rank `rank` of 2^level holds its
+    shard's rows (A_local, B_local).  Construction all-gathers the leaf-norm
+    tables into global norm-only matrices (the cached norms, as the resident
+    matrices cache theirs); allgather(list_of_arrays) -> per-rank lists."""
+
+    def __init__(self, ctx, A_local, B_local, level: int, rank: int, allgather):
+        self.ctx, self.A, self.B = ctx, A_local, B_local
+        self.level, self.rank = level, rank
+        self.allgather = allgather
+        self.n, self.L = A_local.dimension, A_local.leaf_size
+        ta = merge_tables(allgather(list(leaf_table(A_local))))
+        tb = ta if B_local is A_local else merge_tables(allgather(list(leaf_table(B_local))))
+        self.A_norms = nat.from_leaf_norms(ctx, self.n, self.L, *ta)
+        self.B_norms = (self.A_norms if B_local is A_local
+                        else nat.from_leaf_norms(ctx, self.n, self.L, *tb))
+
+    def controlled_product(self, delta: float, taus, fetch, panel_rows: int = 8):
+        """This rank's rows of spamm_with_error_control(A, B, delta, taus)."""
+        import numpy as np
+        if not (delta > 0.0):
+            raise ValueError("spamm_with_error_control: delta must be positive")
+        taus = np.ascontiguousarray(taus, np.float64)
+        nat.tolerance_grid_check(taus)
+        level = self.level
+        if level == 0:
+            bounds = nat.cse(self.ctx, self.A_norms, self.B_norms, taus)
+        else:
+            partial = nat.cse_shard(self.ctx, self.A_norms, self.B_norms, taus, level, self.rank)
+            parts = np.stack([p[0] for p in self.allgather([partial])])
+            bounds = nat.cse_finish(level, nat.top_norms(self.A_norms, level),
+                                    nat.top_norms(self.B_norms, level), parts)
+        tau, k = nat.select_tolerance(bounds, taus, delta)
+        plan = nat.Plan(self.ctx, self.A, self.B_norms, tau, level, self.rank,
+                        a_norms=self.A_norms)
+        moved = run_panels(self.ctx, plan, panel_schedule(self.n, self.L, level, panel_rows),
+                           fetch, self.L)
+        C, st = plan.finish()
+        plan.free()
+        return C, {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
+                   "spamm": st, "panel_bytes": moved}, bounds
+
+
 def controlled_product_distributed(ctx, A_local, B_local, delta: float, taus, level: int,
                                    rank: int, allgather, fetch, panel_rows: int = 8):
-    """Rank `rank` of 2^level: C~ rows of its shard for A*B with A and B
-    distributed by block row.  allgather(list_of_arrays) -> per-rank lists
-    (variable lengths); fetch as in run_panels."""
-    import numpy as np
-    if not (delta > 0.0):
-        raise ValueError("spamm_with_error_control: delta must be positive")
-    taus = np.ascontiguousarray(taus, np.float64)
-    nat.tolerance_grid_check(taus)
-    n, L = A_local.dimension, A_local.leaf_size
-    ta = merge_tables(allgather(list(leaf_table(A_local))))
-    tb = merge_tables(allgather(list(leaf_table(B_local))))
-    A_norms = nat.from_leaf_norms(ctx, n, L, *ta)
-    B_norms = nat.from_leaf_norms(ctx, n, L, *tb)
-    partial = nat.cse_shard(ctx, A_norms, B_norms, taus, level, rank)
-    parts = np.stack([p[0] for p in allgather([partial])])
-    bounds = nat.cse_finish(level, nat.top_norms(A_norms, level), nat.top_norms(B_norms, level),
-                            parts)
-    tau, k = nat.select_tolerance(bounds, taus, delta)
-    plan = nat.Plan(ctx, A_local, B_norms, tau, level, rank, a_norms=A_norms)
-    moved = run_panels(ctx, plan, panel_schedule(n, L, level, panel_rows), fetch, L)
-    C, st = plan.finish()
-    plan.free()
-    return C, {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
-               "spamm": st, "panel_bytes": moved}, bounds
+    """One-shot DistributedOperands(...).controlled_product(...)."""
+    ops = DistributedOperands(ctx, A_local, B_local, level, rank, allgather)
+    return ops.controlled_product(delta, taus, fetch, panel_rows)
