@@ -135,6 +135,33 @@ def test_many_taus_and_piece_batches(ctx, port):
         assert bits_equal(nat.cse(ctx, A, A, taus), port.cse(t, t, taus))
 
 
+@pytest.mark.parametrize("n_taus", [1, 2, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129])
+def test_sweep_kernel_variants_every_grid_size(ctx, port, n_taus):
+    """Depth >= 3 trees run the windowed tile kernel for N_tau <= 128 (1-4
+    windows of 32, the F-in-last-column case across windows) and the
+    breakpoint-window kernel above: bounds bit-identical for log-spaced and
+    very fine grids, with null and zero-norm leaves in the tiles."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import geometric_grid, log_grid
+    rng = np.random.default_rng(100 + n_taus)
+    n, L = 700, 16
+    da = _random_case(rng, n, L, 0.7, 25.0)
+    da[:, 100:140] = 0.0                       # null leaves
+    da[200:216, 300:316] = 1e-300 * rng.uniform(size=(16, 16))  # underflowing products
+    db = _random_case(rng, n, L, 0.9, 60.0)
+    la, lb = nat.dense_to_leaves(da, L), nat.dense_to_leaves(db, L)
+    A, B = nat.upload(ctx, n, L, *la), nat.upload(ctx, n, L, *lb)
+    ta, tb = port.build(n, L, *la), port.build(n, L, *lb)
+    grids = [log_grid(n_taus, 10.0, 1e-6) if n_taus > 1 else np.array([1e-2]),
+             geometric_grid(float(np.sqrt(ta.level_norms(0)[0] * tb.level_norms(0)[0])), 0.97,
+                            n_taus)]
+    for taus in grids:
+        assert bits_equal(nat.cse(ctx, A, B, taus), port.cse(ta, tb, taus))
+    # a grid spanning ~2000 binades (no bucket table: other kernels)
+    wide = np.logspace(300, -300, n_taus) if n_taus > 1 else np.array([1.0])
+    assert bits_equal(nat.cse(ctx, A, B, wide), port.cse(ta, tb, wide))
+
+
 def test_run_to_run_determinism(ctx):
     """SPEC determinism (test_multiply.cpp:140-156 analogue): repeated calls are
     bitwise identical."""
