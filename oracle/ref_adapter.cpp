@@ -16,8 +16,13 @@
 #include <vector>
 
 #include "node_ops.hpp"
+#include <sstream>
+#include <string>
+
 #include "spamm/error_control.hpp"
 #include "spamm/execution.hpp"
+#include "spamm/matrix_market.hpp"
+#include "spamm/oracle.hpp"
 #include "spamm/multiply.hpp"
 #include "spamm/purification.hpp"
 #include "spamm/quadtree.hpp"
@@ -396,6 +401,136 @@ std::int64_t ref_survivors(const void* a, const void* b, double tau, std::int32_
   for (std::int64_t i = 0; i < n; ++i)
     for (int c = 0; c < 3; ++c) triples[3 * i + c] = out[i][c];
   return count;
+}
+
+// ---- experiment-side modules ------------------------------
+// status: 0 ok, 1 std::invalid_argument, 2 std::domain_error, 3 other
+static int classify(const std::exception& e) {
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  if (dynamic_cast<const std::domain_error*>(&e)) return 2;
+  return 3;
+}
+
+// spamm::oracle::generate_decay_matrix (oracle.cpp) -> row-major n x n
+int ref_generate_decay(int n, double alpha, double scale, double low, double high,
+                       std::uint64_t seed, double* out) {
+  try {
+    spamm::oracle::DecayModelSpec spec;
+    spec.dimension = n;
+    spec.alpha = alpha;
+    spec.scale = scale;
+    spec.spectral_low = low;
+    spec.spectral_high = high;
+    spec.seed = seed;
+    const auto d = spamm::oracle::generate_decay_matrix(spec);
+    std::memcpy(out, d.data(), d.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+void ref_gershgorin(const double* a, int n, double* lo, double* hi) {
+  spamm::DenseMatrix d(n);
+  std::memcpy(d.data(), a, d.size() * sizeof(double));
+  const auto b = spamm::oracle::gershgorin_bounds(d);
+  *lo = b.first;
+  *hi = b.second;
+}
+
+int ref_density_oracle(const double* fock, int n, int occupation, double* out) {
+  try {
+    spamm::DenseMatrix d(n);
+    std::memcpy(d.data(), fock, d.size() * sizeof(double));
+    const auto p = spamm::oracle::density_matrix_oracle(d, occupation);
+    std::memcpy(out, p.data(), p.size() * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+// spamm::read_matrix_market (matrix_market.cpp:40-94): returns -1 when cap is
+// too small (count written), else the status above (1 invalid_argument, 3
+// runtime_error).
+int ref_mm_read(const char* text, int* dimension, std::int64_t* count, std::int32_t* rows,
+                std::int32_t* cols, double* values, std::int64_t cap) {
+  try {
+    std::istringstream in{std::string(text)};
+    const auto data = spamm::read_matrix_market(in);
+    *dimension = data.dimension;
+    *count = static_cast<std::int64_t>(data.entries.size());
+    if (*count > cap) return -1;
+    for (std::int64_t i = 0; i < *count; ++i) {
+      rows[i] = data.entries[i].row;
+      cols[i] = data.entries[i].col;
+      values[i] = data.entries[i].value;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
+}
+
+// spamm::write_matrix_market (matrix_market.cpp:96-111) of a reference tree;
+// returns the text length (written up to cap bytes)
+std::int64_t ref_mm_write(const void* x, char* buf, std::int64_t cap) {
+  std::ostringstream out;
+  spamm::write_matrix_market(out, static_cast<const RefTree*>(x)->m);
+  const std::string s = out.str();
+  if (buf) std::memcpy(buf, s.data(), static_cast<std::size_t>(std::min<std::int64_t>(cap, s.size())));
+  return static_cast<std::int64_t>(s.size());
+}
+
+// The squaring protocol of run_squaring_experiment (experiment.cpp:92-128;
+// the file itself needs nlohmann/json, absent here) restated over the
+// reference's own calls: per tolerance, square twice with the variant's
+// method and measure the second square against the exact one.
+// rec9 per tolerance: chosen_tau, nnz_in, nnz_mid, nnz_out, nnz_blocks_out,
+// realized_error, status (0 ok / 1 violation), trace, chosen_tau of square 1.
+int ref_squaring(const void* x, int variant, const double* deltas, int n_deltas,
+                 const double* taus, int n_taus, double* rec9) {
+  try {
+    const spamm::ToleranceGrid grid(std::vector<double>(taus, taus + n_taus));
+    const auto v = static_cast<spamm::Variant>(variant);
+    auto square = [&](const QuadTreeMatrix& in, double delta, double* tau,
+                      std::int64_t* nnz_mid) -> QuadTreeMatrix {
+      if (v == spamm::Variant::truncmul) {
+        QuadTreeMatrix p = spamm::multiply_exact(in, in);
+        *nnz_mid = p.nnz();
+        *tau = 0.0;
+        return std::move(spamm::truncate(p, delta).matrix);
+      }
+      const double d = v == spamm::Variant::hybrid ? delta / 2.0 : delta;
+      auto cp = spamm::spamm_with_error_control(in, in, d, grid);
+      *tau = cp.chosen_tau.tau;
+      *nnz_mid = cp.matrix.nnz();
+      if (v == spamm::Variant::spamm) return std::move(cp.matrix);
+      return std::move(spamm::truncate(cp.matrix, d).matrix);
+    };
+    const auto& input = static_cast<const RefTree*>(x)->m;
+    for (int i = 0; i < n_deltas; ++i) {
+      double* o = rec9 + 9 * i;
+      double tau1 = 0.0, tau2 = 0.0;
+      std::int64_t mid1 = 0, mid2 = 0;
+      const QuadTreeMatrix x1 = square(input, deltas[i], &tau1, &mid1);
+      const QuadTreeMatrix x2 = square(x1, deltas[i], &tau2, &mid2);
+      const QuadTreeMatrix exact = spamm::multiply_exact(x1, x1);
+      const double err = spamm::add(x2, exact.scale(-1.0)).frobenius_norm();
+      o[0] = tau2;
+      o[1] = static_cast<double>(x1.nnz());
+      o[2] = static_cast<double>(mid2);
+      o[3] = static_cast<double>(x2.nnz());
+      o[4] = static_cast<double>(x2.nnz_blocks());
+      o[5] = err;
+      o[6] = err < deltas[i] ? 0.0 : 1.0;
+      o[7] = x2.trace();
+      o[8] = tau1;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return classify(e);
+  }
 }
 
 }  // extern "C"
