@@ -62,6 +62,9 @@ def parse():
                    help="distributed: each rank holds only its block rows of A and B; B panels "
                         "are broadcast by their owners (SURVEY 8e, configs 4/5)")
     p.add_argument("--panel-rows", type=int, default=32)
+    p.add_argument("--transport", default="peer", choices=["peer", "broadcast"],
+                   help="distributed operands: B leaves read in place from the owners' memory "
+                        "(CUDA IPC / NVLink, one GEMM) or broadcast in panels")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=4,
@@ -258,7 +261,7 @@ def run_ours(args, dist):
             out = [None] * dist.world
             dist.pg.all_gather_object(out, arrays)
             return out
-        ops = DistributedOperands(ctx, A, A, level, dist.rank, allgather)
+        ops = DistributedOperands(ctx, A, A, level, dist.rank, allgather, args.transport)
         fetch = torch_fetch(dist.backend or "none", dist.rank, A, w.leaf)
     else:
         A = make_matrix(nat, ctx, w)
@@ -335,8 +338,11 @@ def run_ours(args, dist):
                    "tau_grid": "log-spaced [1e-12, 1e-2]", "drop": w.drop,
                    "parallelism": (f"distributed operands x{dist.world} (level {level}): "
                                    f"block-row shards of A and B, all-gathered norm tables, "
-                                   f"B panels of {args.panel_rows} block rows broadcast by "
-                                   f"their owners ({dist.backend or 'local'})"
+                                   + ("B leaves read in place from the owners' memory (CUDA IPC "
+                                      "over NVLink) by one GEMM"
+                                      if args.transport == "peer" else
+                                      f"B panels of {args.panel_rows} block rows broadcast by "
+                                      f"their owners ({dist.backend or 'local'})")
                                    if distributed else
                                    f"row-shards x{dist.world} (level {level}), "
                                    f"{dist.backend} all-gather of level-{level} CSE vectors"
@@ -380,6 +386,8 @@ def run_ours(args, dist):
         out["e2e"], host = run_e2e(args, nat, ctx, stream, A, w, taus)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline and not distributed:
         out["cpu_baseline"] = run_cpu_baseline(args, nat, A, w, taus, st["tau"], host)
+    if distributed:  # every rank done reading the others' B before any unmaps
+        ops.close(barrier=dist.barrier if dist.world > 1 else None)
     return out
 
 

@@ -323,6 +323,22 @@ int spg_plan_accumulate(spg_plan* plan, int32_t row_begin, int32_t row_end,
                         const double* d_panel, void* stream);
 int spg_plan_finish(spg_plan* plan, spg_matrix** c, spg_spamm_stats* stats);
 void spg_plan_free(spg_plan* plan);
+/* All of the plan's products in ONE GEMM launch, B leaf t read in place
+ * from owner_base[slot_owner[t]] + slot_local[t] * L*L: the owners' leaf
+ * payloads, local or another GPU's memory opened with spg_ipc_open (NVLink
+ * peer loads inside the GEMM -- no staging copy, no broadcast).  Host arrays
+ * of B's leaf count (slots of the norm-only B); replaces the panels. */
+int spg_plan_run_table(spg_plan* plan, int32_t n_owners, const double* const* owner_base,
+                       const int32_t* slot_owner, const int32_t* slot_local, void* stream);
+/* Device address of a matrix's leaf payload (slot t at base + t * L*L). */
+int spg_matrix_payload(const spg_matrix* m, const double** base);
+/* Payload slot of every non-null leaf, in spg_matrix_download order. */
+int spg_matrix_payload_slots(const spg_matrix* m, int32_t* slots);
+/* CUDA IPC of a matrix's leaf payload (64-byte handle) for the processes of
+ * one node; the exporting matrix must outlive every importer's use. */
+int spg_ipc_export(const spg_matrix* m, void* handle);
+int spg_ipc_open(spg_context* ctx, const void* handle, const double** base);
+int spg_ipc_close(spg_context* ctx, const double* base);
 /* Norm-only matrix from a leaf table (host arrays, sorted by block row; slot
  * t = leaf t).  nonzero may be NULL (every leaf non-null).  Norms are taken
  * as given: pass the block_norm values the owning GPU computed (download

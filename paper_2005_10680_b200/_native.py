@@ -164,6 +164,12 @@ _SIGNATURES = {
     "spg_plan_accumulate": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp]),
     "spg_plan_finish": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(SpammStats)]),
     "spg_plan_free": (None, [_vp]),
+    "spg_plan_run_table": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), _i32p, _i32p, _vp]),
+    "spg_matrix_payload": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "spg_matrix_payload_slots": (C.c_int, [_vp, _i32p]),
+    "spg_ipc_export": (C.c_int, [_vp, C.c_char_p]),
+    "spg_ipc_open": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
+    "spg_ipc_close": (C.c_int, [_vp, _vp]),
     "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
                                              _dp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
     "spg_matrix_gather_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64, _vp]),
@@ -324,6 +330,17 @@ class Matrix:
         n = self.info().dimension
         out = np.empty((n, n), np.float64)
         _check(lib().spg_matrix_to_dense(self._h, _ptr(out, C.c_double)))
+        return out
+
+    def payload_ptr(self) -> int:
+        p = _vp()
+        _check(lib().spg_matrix_payload(self._h, C.byref(p)))
+        return p.value or 0
+
+    def payload_slots(self) -> np.ndarray:
+        """Payload slot per non-null leaf, aligned with download()."""
+        out = np.empty(self.info().nnz_blocks, np.int32)
+        _check(lib().spg_matrix_payload_slots(self._h, _ptr(out, C.c_int32)))
         return out
 
     def level_norms(self, level: int) -> np.ndarray:
@@ -665,6 +682,15 @@ class Plan:
         address the panel was produced on (stream-ordered hand-off)."""
         _check(lib().spg_plan_accumulate(self._h, r0, r1, d_panel or None, stream or None))
 
+    def run_table(self, owner_bases, slot_owner, slot_local, stream: int | None = None):
+        """Every product in one GEMM, B leaf t read at owner_bases[slot_owner[t]]
+        + slot_local[t] L^2 (device addresses; peers' via ipc_open)."""
+        so = np.ascontiguousarray(slot_owner, np.int32)
+        sl = np.ascontiguousarray(slot_local, np.int32)
+        bases = (_vp * max(len(owner_bases), 1))(*[_vp(b) for b in owner_bases])
+        _check(lib().spg_plan_run_table(self._h, len(owner_bases), bases, _ptr(so, C.c_int32),
+                                        _ptr(sl, C.c_int32), stream or None))
+
     def finish(self):
         h = _vp()
         st = SpammStats()
@@ -706,6 +732,22 @@ def gather_rows(m: Matrix, r0: int, r1: int, d_out: int, capacity: int,
     """Non-null leaves of block rows [r0, r1) in (row, col) order -> d_out."""
     _check(lib().spg_matrix_gather_rows(m.handle, r0, r1, d_out or None, capacity,
                                         stream or None))
+
+
+def ipc_export(m: Matrix) -> bytes:
+    buf = C.create_string_buffer(64)
+    _check(lib().spg_ipc_export(m.handle, buf))
+    return buf.raw
+
+
+def ipc_open(ctx: Context, handle: bytes) -> int:
+    p = _vp()
+    _check(lib().spg_ipc_open(ctx.handle, bytes(handle), C.byref(p)))
+    return p.value
+
+
+def ipc_close(ctx: Context, ptr: int):
+    _check(lib().spg_ipc_close(ctx.handle, _vp(ptr)))
 
 
 def sort_by_block_row(rows, cols, payload):

@@ -98,6 +98,7 @@ struct spg_matrix {
   double* pyramid = nullptr;    // sum_l 4^l
   double frob = 0.0;
   bool norms_only = false;      // norms of a host-resident B (spg_bstream): no payload
+  const double** leaf_ptrs = nullptr;  // n_slots leaf addresses (GEMM B table), built on first use
   // norms_only: leaves (slots) sorted by block row; slots of block rows
   // [r0, r1) are [row_slot_begin[r0], row_slot_begin[r1]) (2^depth + 1 entries)
   std::vector<int64_t> row_slot_begin;
@@ -261,6 +262,9 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
                          HostOut* host = nullptr);
 
 int64_t copy_scalar_to_host_i64(spg_context* ctx, const int64_t* d);
+// the matrix's leaf address table (payload + t L^2), built once on ctx->stream
+const double* const* leaf_table(spg_context* ctx, const spg_matrix* m);
+__global__ void leaf_ptr_kernel(const double* payload, int64_t n, int64_t LL, const double** out);
 
 // the product with B streamed panel by panel from host memory; C identical
 // (bitwise) to spamm_device with B resident

@@ -271,9 +271,28 @@ __global__ void panel_gather(const double* __restrict__ payload,
 
 }  // namespace
 
+__global__ void leaf_ptr_kernel(const double* payload, int64_t n, int64_t LL,
+                                const double** out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < n) out[t] = payload + t * LL;
+}
+
+const double* const* leaf_table(spg_context* ctx, const spg_matrix* m) {
+  if (!m->payload || m->n_slots == 0) return nullptr;
+  auto* mm = const_cast<spg_matrix*>(m);  // cache: built once, read-only afterwards
+  if (!mm->leaf_ptrs) {
+    mm->leaf_ptrs = dev_alloc<const double*>(m->n_slots, ctx);
+    leaf_ptr_kernel<<<grid_for(m->n_slots, 256), 256, 0, ctx->stream>>>(
+        m->payload, m->n_slots, static_cast<int64_t>(m->leaf) * m->leaf, mm->leaf_ptrs);
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  return mm->leaf_ptrs;
+}
+
 void matrix_destroy(spg_matrix* m) {
   if (!m) return;
   spg_context* ctx = m->ctx;
+  dev_free(m->leaf_ptrs, ctx);
   m->payload_ref.reset();  // returns the payload to the pool with its last user
   dev_free(m->keys, ctx);
   dev_free(m->slots, ctx);
@@ -742,6 +761,59 @@ int spg_matrix_gather_rows(const spg_matrix* m, int32_t row_begin, int32_t row_e
     SPG_CUDA(cudaStreamWaitEvent(foreign, ev, 0));
     cudaEventDestroy(ev);  // released once the recorded work completes
   }
+  SPG_API_END
+}
+
+
+int spg_matrix_payload(const spg_matrix* m, const double** base) {
+  SPG_API_BEGIN
+  if (!m || !base) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
+  *base = m->payload;
+  SPG_API_END
+}
+
+int spg_matrix_payload_slots(const spg_matrix* m, int32_t* slots) {
+  SPG_API_BEGIN
+  if (!m || !slots) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
+  CtxGuard g(m->ctx);
+  if (m->nnzb)
+    SPG_CUDA(cudaMemcpyAsync(slots, m->slots, m->nnzb * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             m->ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(m->ctx->stream));
+  SPG_API_END
+}
+
+int spg_ipc_export(const spg_matrix* m, void* handle) {
+  SPG_API_BEGIN
+  if (!m || !handle) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
+  if (!m->payload) fail(SPG_EINVAL, "matrix has no leaves to export");
+  CtxGuard g(m->ctx);
+  cudaIpcMemHandle_t h;
+  SPG_CUDA(cudaIpcGetMemHandle(&h, m->payload));
+  std::memcpy(handle, &h, sizeof h);
+  SPG_API_END
+}
+
+int spg_ipc_open(spg_context* ctx, const void* handle, const double** base) {
+  SPG_API_BEGIN
+  if (!ctx || !handle || !base) fail(SPG_EINVAL, "null argument");
+  CtxGuard g(ctx);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* p = nullptr;
+  SPG_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *base = static_cast<const double*>(p);
+  SPG_API_END
+}
+
+int spg_ipc_close(spg_context* ctx, const double* base) {
+  SPG_API_BEGIN
+  if (!ctx || !base) fail(SPG_EINVAL, "null argument");
+  CtxGuard g(ctx);
+  SPG_CUDA(cudaIpcCloseMemHandle(const_cast<double*>(base)));
   SPG_API_END
 }
 

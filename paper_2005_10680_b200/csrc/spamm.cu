@@ -228,14 +228,15 @@ int64_t count_candidates(spg_context* ctx, const spg_matrix* a, const spg_matrix
 template <int L, int KC, int WM, int WN, int NSTAGE>
 void launch_dmma(spg_context* ctx, const double* A, const double* B, const int2* pairs,
                  const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st,
-                 const int64_t* out_end, int accumulate) {
+                 const int64_t* out_end, int accumulate, const double* const* btab) {
   using Cfg = DmmaGemmCfg<L, KC, WM, WN, NSTAGE>;
-  auto kern = leaf_gemm_dmma<L, KC, WM, WN, NSTAGE>;
+  auto kern = btab ? leaf_gemm_dmma<L, KC, WM, WN, NSTAGE, true>
+                   : leaf_gemm_dmma<L, KC, WM, WN, NSTAGE, false>;
   SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Cfg::kSmemBytes)));
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
   kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, st>>>(A, B, pairs, out_offset, n_out, C, out_end,
-                                                     accumulate);
+                                                     accumulate, btab);
   SPG_CHECK_LAUNCH(ctx);
 }
 
@@ -268,33 +269,35 @@ int gemm_variant() {
 
 void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const int2* pairs,
               const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st = nullptr,
-              const int64_t* out_end = nullptr, int accumulate = 0) {
+              const int64_t* out_end = nullptr, int accumulate = 0,
+              const double* const* btab = nullptr) {
   if (n_out == 0) return;
   if (!st) st = ctx->stream;
-  if ((out_end || accumulate) && L == 64 && gemm_variant() == 3)
-    fail(SPG_EINVAL, "panel accumulation is not supported by the TMA variant");
+  if ((out_end || accumulate || btab) && L == 64 && gemm_variant() == 3)
+    fail(SPG_EINVAL, "panels / leaf tables are not supported by the TMA variant");
   if (L == 64 && gemm_variant() == 3) {
     launch_tma64<3>(ctx, A, B, pairs, out_offset, n_out, C, st);
     return;
   }
   if (L == 64 && gemm_variant() == 4) {  // 4 warps x 32x32, 2 stages, 3 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
     return;
   }
   if (L == 64 && gemm_variant() == 5) {  // 4 warps x 32x32, 3 stages, 2 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate,
+                                   btab);
     return;
   }
   if (L == 64 && gemm_variant() == 6) {  // 4 warps x 32x32, KC=16, 4 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
     return;
   }
   if (L == 64 && gemm_variant() == 8) {  // 4 warps x 32x32, KC=16, 3 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+    launch_dmma<64, 16, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
     return;
   }
   if (L == 64 && gemm_variant() == 7) {  // 4 warps x 32x32, KC=16, 6 stages, 2 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
     return;
   }
   switch (L) {
@@ -303,23 +306,23 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
         const char* e = std::getenv("SPG_GEMM32");  // developer switch for the L=32 tiling
         return e ? std::atoi(e) : 2;
       }();
-      if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
-      else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
-      else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
-      else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
-      else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       break;
     }
     case 64:
-      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       break;
     case 128:
-      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate);
+      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       break;
     default: {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
       leaf_gemm_generic<<<grid, 256, 0, st>>>(A, B, pairs, out_offset, n_out, L, C, out_end,
-                                              accumulate);
+                                              accumulate, btab);
       SPG_CHECK_LAUNCH(ctx);
     }
   }
@@ -387,6 +390,7 @@ Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
 void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
                             DevBuf<int2>& pairs, DevBuf<int64_t>& out_offset,
                             DevBuf<uint64_t>& out_keys, int64_t n_out, HostOut* host) {
+  const double* const* btab = leaf_table(ctx, b);  // before the aux stream forks
   const int L = a->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
   if (n_out > host->capacity) fail(SPG_EINVAL, "output capacity smaller than the product");
@@ -431,11 +435,11 @@ void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_mat
       cudaStream_t st = cs_[c & 1];
       if (dbg == 2) {  // no copies at all
         run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get() + o0, o1 - o0,
-                 c_payload.get() + o0 * LL, st);
+                 c_payload.get() + o0 * LL, st, nullptr, 0, btab);
         continue;
       }
       run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get() + o0, o1 - o0,
-               c_payload.get() + o0 * LL, st);
+               c_payload.get() + o0 * LL, st, nullptr, 0, btab);
       leaf_norms(ctx, c_payload.get() + o0 * LL, o1 - o0, L, a->dimension, nb, nullptr, nullptr,
                  norms.get() + o0, nz.get() + o0, nullptr, st);
       SPG_CUDA(cudaEventRecord(done[c], st));
@@ -506,9 +510,11 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   } else {
     double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+    const double* const* btab = leaf_table(ctx, b);
     {
       PhaseTrace tr(ctx, "gemm");
-      run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload);
+      run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload,
+               nullptr, nullptr, 0, btab);
     }
     SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
     pairs.reset();
@@ -582,6 +588,7 @@ struct spg_plan {
   spg::Plan pl;
   spg::DevBuf<double> c;
   spg::DevBuf<int64_t> beg, end;
+  spg::DevBuf<const double*> btab;  // B leaf addresses of the panels seen so far
   int32_t next_row = 0;
   bool finished = false;
   spg_spamm_stats stats{};
@@ -631,6 +638,7 @@ spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b
   if (n_out) SPG_CUDA(cudaMemsetAsync(plan->c.get(), 0, n_out * LL * sizeof(double), ctx->stream));
   plan->beg = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
   plan->end = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
+  plan->btab = DevBuf<const double*>(std::max<int64_t>(b->n_slots, 1), ctx);
   SPG_CUDA(cudaEventSynchronize(ctx->ev[3]));
   spg_spamm_stats& st = plan->stats;
   st.survivors = plan->pl.n_surv;
@@ -669,8 +677,32 @@ void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_pan
       static_cast<uint32_t>(r0), static_cast<uint32_t>(r1), plan->beg.get(), plan->end.get());
   SPG_CHECK_LAUNCH(ctx);
   // pairs hold B slots; the panel buffer starts at slot lo
-  run_gemm(ctx, L, plan->a->payload, d_panel - lo * LL, plan->pl.pairs.get(), plan->beg.get(),
-           n_out, plan->c.get(), ctx->stream, plan->end.get(), 1);
+  leaf_ptr_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(d_panel, cnt, LL,
+                                                              plan->btab.get() + lo);
+  SPG_CHECK_LAUNCH(ctx);
+  run_gemm(ctx, L, plan->a->payload, nullptr, plan->pl.pairs.get(), plan->beg.get(), n_out,
+           plan->c.get(), ctx->stream, plan->end.get(), 1, plan->btab.get());
+}
+
+// Every product at once, B leaf t read from btab[t] (one GEMM launch; the
+// leaves may live in other GPUs' memory mapped over NVLink).
+void plan_run_table(spg_plan* plan, const double* const* h_table, int64_t n_table) {
+  spg_context* ctx = plan->ctx;
+  if (plan->finished) fail(SPG_EINVAL, "plan: already finished");
+  if (plan->next_row != 0) fail(SPG_EINVAL, "plan: panels already accumulated");
+  if (n_table != plan->b->n_slots) fail(SPG_EINVAL, "plan: leaf table size != B leaf count");
+  const int32_t nbp = 1 << plan->b->depth;
+  plan->next_row = nbp;
+  const int64_t n_out = plan->pl.n_out;
+  if (n_out == 0) return;
+  DevBuf<const double*> d_tab(std::max<int64_t>(n_table, 1), ctx);
+  SPG_CUDA(cudaMemcpyAsync(d_tab.get(), h_table, n_table * sizeof(const double*),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  SPG_CUDA(cudaEventRecord(plan->t_first, ctx->stream));
+  plan->started = true;
+  run_gemm(ctx, plan->a->leaf, plan->a->payload, nullptr, plan->pl.pairs.get(),
+           plan->pl.out_offset.get(), n_out, plan->c.get(), ctx->stream, nullptr, 0, d_tab.get());
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));  // the table buffer returns to the pool
 }
 
 spg_matrix* plan_finish(spg_plan* plan) {
@@ -1034,6 +1066,27 @@ int spg_plan_finish(spg_plan* plan, spg_matrix** c, spg_spamm_stats* stats) {
   CtxGuard g(plan->ctx);
   *c = plan_finish(plan);
   if (stats) *stats = plan->stats;
+  SPG_API_END
+}
+
+int spg_plan_run_table(spg_plan* plan, int32_t n_owners, const double* const* owner_base,
+                       const int32_t* slot_owner, const int32_t* slot_local, void* stream) {
+  SPG_API_BEGIN
+  if (!plan || (n_owners > 0 && !owner_base)) fail(SPG_EINVAL, "null argument");
+  const int64_t n = plan->b->n_slots;
+  if (n > 0 && (!slot_owner || !slot_local)) fail(SPG_EINVAL, "null argument");
+  const int64_t LL = static_cast<int64_t>(plan->b->leaf) * plan->b->leaf;
+  std::vector<const double*> tab(static_cast<size_t>(n));
+  for (int64_t t = 0; t < n; ++t) {
+    const int32_t o = slot_owner[t];
+    if (o < 0 || o >= n_owners || slot_local[t] < 0)
+      fail(SPG_EINVAL, "plan: leaf table entry outside the owners");
+    tab[t] = owner_base[o] + static_cast<int64_t>(slot_local[t]) * LL;
+  }
+  CtxGuard g(plan->ctx);
+  ForeignOrder fo(plan->ctx, stream, plan->ev[0]);
+  plan_run_table(plan, tab.data(), n);
+  fo.done();
   SPG_API_END
 }
 

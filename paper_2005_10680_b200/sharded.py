@@ -150,20 +150,68 @@ class DistributedOperands:
     """A and B distributed by block row: rank `rank` of 2^level holds its
     shard's rows (A_local, B_local).  Construction all-gathers the leaf-norm
     tables into global norm-only matrices (the cached norms, as the resident
-    matrices cache theirs); allgather(list_of_arrays) -> per-rank lists."""
+    matrices cache theirs); allgather(list_of_arrays) -> per-rank lists.
 
-    def __init__(self, ctx, A_local, B_local, level: int, rank: int, allgather):
+    transport "broadcast": B panels are broadcast by their owners (run_panels
+    with a fetch()); "peer": every rank maps the other ranks' B payloads into
+    its address space (CUDA IPC; over NVLink between GPUs) and ONE GEMM reads
+    each B leaf in place (spg_plan_run_table) -- the all-gather fused into the
+    product, no staging buffers.  Ranks must call close() together."""
+
+    def __init__(self, ctx, A_local, B_local, level: int, rank: int, allgather,
+                 transport: str = "broadcast"):
+        import numpy as np
+        if transport not in ("broadcast", "peer"):
+            raise ValueError("transport must be 'broadcast' or 'peer'")
         self.ctx, self.A, self.B = ctx, A_local, B_local
         self.level, self.rank = level, rank
         self.allgather = allgather
+        self.transport = transport
         self.n, self.L = A_local.dimension, A_local.leaf_size
+        self.opened = []
         ta = merge_tables(allgather(list(leaf_table(A_local))))
+        if transport == "peer":
+            # B table with (owner, payload slot) per leaf, merged in (row, col) order
+            r, c, _, nrm = B_local.download(payload=False)
+            sl = B_local.payload_slots() if len(r) else np.empty(0, np.int32)
+            handle = nat.ipc_export(B_local) if len(r) else bytes(64)
+            parts = allgather([r, c, nrm, sl, np.frombuffer(handle, np.uint8)])
+            owner = np.concatenate([np.full(len(p[0]), k, np.int32) for k, p in enumerate(parts)])
+            rows = np.concatenate([p[0] for p in parts]).astype(np.int32)
+            cols = np.concatenate([p[1] for p in parts]).astype(np.int32)
+            norms = np.concatenate([p[2] for p in parts]).astype(np.float64)
+            local = np.concatenate([p[3] for p in parts]).astype(np.int32)
+            order = np.lexsort((cols, rows))
+            tb = (rows[order], cols[order], norms[order])
+            self.slot_owner, self.slot_local = owner[order], local[order]
+            self.bases = []
+            for k, p in enumerate(parts):
+                if k == rank:
+                    self.bases.append(B_local.payload_ptr() if len(r) else 0)
+                elif len(p[0]):
+                    ptr = nat.ipc_open(ctx, p[4].tobytes())
+                    self.opened.append(ptr)
+                    self.bases.append(ptr)
+                else:
+                    self.bases.append(0)
+            self.A_norms = nat.from_leaf_norms(ctx, self.n, self.L, *ta)
+            self.B_norms = nat.from_leaf_norms(ctx, self.n, self.L, *tb)
+            return
         tb = ta if B_local is A_local else merge_tables(allgather(list(leaf_table(B_local))))
         self.A_norms = nat.from_leaf_norms(ctx, self.n, self.L, *ta)
         self.B_norms = (self.A_norms if B_local is A_local
                         else nat.from_leaf_norms(ctx, self.n, self.L, *tb))
 
-    def controlled_product(self, delta: float, taus, fetch, panel_rows: int = 8):
+    def close(self, barrier=None):
+        """Unmap the peers' payloads; with `barrier`, first wait until every
+        rank is done reading this rank's B."""
+        if barrier is not None:
+            barrier()
+        for ptr in self.opened:
+            nat.ipc_close(self.ctx, ptr)
+        self.opened = []
+
+    def controlled_product(self, delta: float, taus, fetch=None, panel_rows: int = 8):
         """This rank's rows of spamm_with_error_control(A, B, delta, taus)."""
         import numpy as np
         if not (delta > 0.0):
@@ -181,8 +229,13 @@ class DistributedOperands:
         tau, k = nat.select_tolerance(bounds, taus, delta)
         plan = nat.Plan(self.ctx, self.A, self.B_norms, tau, level, self.rank,
                         a_norms=self.A_norms)
-        moved = run_panels(self.ctx, plan, panel_schedule(self.n, self.L, level, panel_rows),
-                           fetch, self.L)
+        if self.transport == "peer":
+            plan.run_table(self.bases, self.slot_owner, self.slot_local)
+            mine = self.slot_owner == self.rank
+            moved = int((~mine).sum()) * self.L * self.L * 8  # upper bound: leaves read remotely
+        else:
+            moved = run_panels(self.ctx, plan,
+                               panel_schedule(self.n, self.L, level, panel_rows), fetch, self.L)
         C, st = plan.finish()
         plan.free()
         return C, {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,

@@ -9,8 +9,12 @@ the whole matrices.
 * CPU: panel schedule and table merge (host logic).
 * GPU, one process: every shard's plan fed from its owners' matrices through
   spg_matrix_gather_rows (the broadcast replaced by a direct read).
+* GPU, one process: the one-GEMM leaf-table path (spg_plan_run_table) with B
+  split over two owner allocations.
 * GPU, two processes (gloo, host-side collectives; the ranks time-share the
-  one GPU and never wait on each other's kernels): the full driver."""
+  one GPU and never wait on each other's kernels): the full driver, with B
+  panels broadcast by their owners or read in place from the other process's
+  memory through CUDA IPC (transport "peer")."""
 import os
 import socket
 
@@ -142,6 +146,46 @@ def test_plan_contract_errors(ctx):
         nat.from_leaf_norms(ctx, n, L, r[::-1], c[::-1], nr[::-1])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("L", [16, 32, 64, 128])
+def test_plan_leaf_table_one_gemm_bitwise(ctx, L):
+    """spg_plan_run_table: every product in one GEMM with B leaves read through
+    a per-leaf address table (the NVLink peer path's kernel) == resident
+    product, bitwise; B split over two owner allocations."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    n = 40 * L // 4 + 3
+    A = nat.synth_cluster_device(ctx, n - n % 4, L, 3.0, 0.1, 2005, 1, 1e-10)
+    n = A.dimension
+    nb = -(-n // L)
+    half = nb // 2
+    Bs = [nat.synth_cluster_device_rows(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10, 0, half),
+          nat.synth_cluster_device_rows(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10, half, nb)]
+    B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10)
+    rows, cols, norms, owner, local = [], [], [], [], []
+    for k, M in enumerate(Bs):
+        r, c, _, nr = M.download(payload=False)
+        rows.append(r); cols.append(c); norms.append(nr)
+        owner.append(np.full(len(r), k, np.int32)); local.append(M.payload_slots())
+    rows, cols, norms = (np.concatenate(x) for x in (rows, cols, norms))
+    owner, local = np.concatenate(owner), np.concatenate(local)
+    order = np.lexsort((cols, rows))
+    Bn = nat.from_leaf_norms(ctx, n, L, rows[order], cols[order], norms[order])
+    taus = log_grid(32)
+    bounds = nat.cse(ctx, A, B, taus)
+    assert bits_equal(nat.cse(ctx, A, Bn, taus), bounds)
+    for tau in (nat.select_tolerance(bounds, taus, 1e-6)[0], 0.0):
+        plan = nat.Plan(ctx, A, Bn, tau)
+        plan.run_table([M.payload_ptr() for M in Bs], owner[order], local[order])
+        C1, s1 = plan.finish()
+        C0, s0 = nat.spamm(ctx, A, B, tau)
+        r0, c0, p0, n0 = C0.download()
+        r1, c1, p1, n1 = C1.download()
+        assert np.array_equal(r0, r1) and np.array_equal(c0, c1)
+        assert bits_equal(p0, p1) and bits_equal(n0, n1)
+        assert s0["survivors"] == s1["survivors"]
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -184,12 +228,50 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
+def _peer_worker(rank, world, port, out_dir):
+    import sys
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    from paper_2005_10680_b200.sharded import DistributedOperands
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ctx = nat.Context(0)
+    n, L, level = 2048, 64, 1
+    nb = n // L
+    lo, hi = rank * nb // world, (rank + 1) * nb // world
+    A = nat.synth_cluster_device_rows(ctx, n, L, 3.0, 0.1, 2005, 1, 1e-10, lo, hi)
+    B = nat.synth_cluster_device_rows(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10, lo, hi)
+
+    def allgather(arrays):
+        out = [None] * world
+        dist.all_gather_object(out, arrays)
+        return out
+
+    ops = DistributedOperands(ctx, A, B, level, rank, allgather, transport="peer")
+    C, st, bounds = ops.controlled_product(1e-6, log_grid(32))
+    r, c, p, nrm = C.download()
+    ops.close(barrier=dist.barrier)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), r=r, c=c, p=p, n=nrm, bounds=bounds,
+             tau=st["tau"], surv=st["spamm"]["survivors"])
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 @pytest.mark.gpu
-def test_two_ranks_gloo_distributed_driver(ctx, tmp_path):
+@pytest.mark.parametrize("transport", ["broadcast", "peer"])
+def test_two_ranks_gloo_distributed_driver(ctx, tmp_path, transport):
+    """Two processes on the one GPU, host-side (gloo) collectives; 'peer' maps
+    the other process's B payload with CUDA IPC and reads it inside the GEMM."""
     import torch.multiprocessing as mp
     from paper_2005_10680_b200 import _native as nat
     from paper_2005_10680_b200.inputs import log_grid
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    worker = _peer_worker if transport == "peer" else _worker
+    mp.spawn(worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
     n, L = 2048, 64
     A = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 1, 1e-10)
     B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10)
