@@ -395,7 +395,11 @@ def run_e2e(args, nat, ctx, stream, A, w, taus):
     """The controlled product through the C ABI with pinned host buffers:
     every step uploads A (leaf coordinates + payload, H2D), runs
     spg_spamm_with_error_control, and downloads C (coordinates, payload,
-    norms, D2H)."""
+    norms, D2H).  `value`: the steps pipelined -- step i+1's input is staged
+    (spg_matrix_stage, upload stream) while step i's product runs and streams
+    C out (copy stream), so both directions of the host link overlap the
+    GEMM; every step's copies stay inside the timed region.  `serial`: the
+    same steps one after the other (upload, then product)."""
     import ctypes as C
     import torch
     rows, cols, pay, _ = A.download(payload=True)
@@ -411,42 +415,69 @@ def run_e2e(args, nat, ctx, stream, A, w, taus):
     o_pay = torch.empty((cap, LL), dtype=torch.float64).pin_memory()
     lib = nat.lib()
     i32p, dp = C.POINTER(C.c_int32), C.POINTER(C.c_double)
+    outs = (o_rows.numpy(), o_cols.numpy(), o_pay.numpy(), o_norm.numpy())
 
-    def step():
+    def upload():
         h = C.c_void_p()
         nat._check(lib.spg_matrix_upload(ctx.handle, w.n, w.leaf, n,
                                          C.cast(h_rows.data_ptr(), i32p),
                                          C.cast(h_cols.data_ptr(), i32p),
                                          C.cast(h_pay.data_ptr(), dp), C.byref(h)))
-        Ah = nat.Matrix(ctx, h)
+        return nat.Matrix(ctx, h)
+
+    def stage():
+        return nat.Staged(ctx, w.n, w.leaf, n, h_rows.data_ptr(), h_cols.data_ptr(),
+                          h_pay.data_ptr())
+
+    def product(Ah):
         # the controlled product with C streamed into the pinned host buffers
         # while the GEMM runs (spg_spamm_with_error_control_to_host)
-        out, st, _ = nat.spamm_with_error_control_to_host(
-            ctx, Ah, Ah, w.delta, taus,
-            out=(o_rows.numpy(), o_cols.numpy(), o_pay.numpy(), o_norm.numpy()))
-        nout = len(out[0])
-        d2h = nout * (LL * 8 + 4 + 4 + 8)
-        return st, d2h
+        out, st, _ = nat.spamm_with_error_control_to_host(ctx, Ah, Ah, w.delta, taus, out=outs)
+        return st, len(out[0]) * (LL * 8 + 4 + 4 + 8)
 
-    for _ in range(max(1, min(args.warmup, 2))):
-        step()
-    ctx.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    flops = 0.0
-    d2h = 0
-    for _ in range(args.steps):
-        st, d2h = step()
-        flops += st["spamm"]["flops"]
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    def timed(run_steps, k):
+        ctx.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        flops, d2h = run_steps(k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        return ev0.elapsed_time(ev1), flops, d2h
+
+    def serial(k):
+        flops, d2h = 0.0, 0
+        for _ in range(k):
+            st, d2h = product(upload())
+            flops += st["spamm"]["flops"]
+        return flops, d2h
+
+    def pipelined(k):
+        flops, d2h = 0.0, 0
+        staged = stage()
+        for i in range(k):
+            Ah = staged.finish()
+            staged = stage() if i + 1 < k else None
+            st, d2h = product(Ah)
+            del Ah
+            flops += st["spamm"]["flops"]
+        return flops, d2h
+
+    warm = max(1, min(args.warmup, 2))
+    serial(warm)
+    ms_s, flops_s, _ = timed(serial, args.steps)
+    pipelined(warm)
+    ms, flops, d2h = timed(pipelined, args.steps)
     h2d = n * (LL * 8 + 4 + 4)
     return ({"value": round(flops / (ms / 1e3) / 1e12, 4), "unit": "TFLOP/s",
              "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
              "ms_per_step": round(ms / args.steps, 3),
-             "path": "C ABI: spg_matrix_upload (pinned H2D) -> "
-                     "spg_spamm_with_error_control_to_host (C streamed D2H during the GEMM)"},
+             "path": "C ABI: spg_matrix_stage (pinned H2D of step i+1 on the upload stream) -> "
+                     "spg_matrix_stage_finish -> spg_spamm_with_error_control_to_host (C "
+                     "streamed D2H during the GEMM)",
+             "serial": {"value": round(flops_s / (ms_s / 1e3) / 1e12, 4),
+                        "ms_per_step": round(ms_s / args.steps, 3),
+                        "path": "spg_matrix_upload then the product, no overlap"}},
             (rows, cols, pay))
 
 

@@ -95,6 +95,19 @@ int spg_matrix_upload(spg_context* ctx, int32_t dimension, int32_t leaf_size, in
                       const int32_t* block_rows, const int32_t* block_cols, const double* payload,
                       spg_matrix** out);
 /* Same with device-resident inputs (the matrix takes a private copy). */
+/* Staged upload: the same as spg_matrix_upload, split in two.  stage()
+ * queues the host->device copies on the context's upload stream and returns
+ * at once (the pinned host buffers must stay unchanged until the matching
+ * stage_finish() returns); stage_finish() makes the context's work wait for
+ * the copies and builds the matrix (norms, pyramid).  Lets a caller stream
+ * the next input in while the current product runs.  stage_finish() (or
+ * spg_staged_free()) releases the staging object. */
+typedef struct spg_staged spg_staged;
+int spg_matrix_stage(spg_context* ctx, int32_t dimension, int32_t leaf_size, int64_t n_leaves,
+                     const int32_t* block_rows, const int32_t* block_cols, const double* payload,
+                     spg_staged** out);
+int spg_matrix_stage_finish(spg_staged* staged, spg_matrix** out);
+void spg_staged_free(spg_staged* staged);
 int spg_matrix_upload_device(spg_context* ctx, int32_t dimension, int32_t leaf_size,
                              int64_t n_leaves, const int32_t* d_block_rows,
                              const int32_t* d_block_cols, const double* d_payload,

@@ -170,6 +170,10 @@ _SIGNATURES = {
     "spg_ipc_export": (C.c_int, [_vp, C.c_char_p]),
     "spg_ipc_open": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
     "spg_ipc_close": (C.c_int, [_vp, _vp]),
+    "spg_matrix_stage": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _vp, _vp, _vp,
+                                   C.POINTER(_vp)]),
+    "spg_matrix_stage_finish": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "spg_staged_free": (None, [_vp]),
     "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
                                              _dp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
     "spg_matrix_gather_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64, _vp]),
@@ -374,6 +378,32 @@ def upload(ctx: Context, dimension: int, leaf_size: int, rows, cols, payload) ->
     _check(lib().spg_matrix_upload(ctx.handle, dimension, leaf_size, n, _ptr(rows, C.c_int32),
                                    _ptr(cols, C.c_int32), _ptr(payload, C.c_double), C.byref(h)))
     return Matrix(ctx, h)
+
+
+class Staged:
+    """spg_matrix_stage: host->device copies queued on the context's upload
+    stream; finish() builds the matrix.  rows/cols/payload: host addresses of
+    pinned buffers that stay unchanged until finish() returns."""
+
+    def __init__(self, ctx: Context, dimension: int, leaf_size: int, n_leaves: int,
+                 rows_ptr: int, cols_ptr: int, payload_ptr: int):
+        self.ctx = ctx
+        self._h = _vp()
+        _check(lib().spg_matrix_stage(ctx.handle, dimension, leaf_size, n_leaves, rows_ptr,
+                                      cols_ptr, payload_ptr, C.byref(self._h)))
+
+    def finish(self) -> "Matrix":
+        h = _vp()
+        st, self._h = self._h, None
+        _check(lib().spg_matrix_stage_finish(st, C.byref(h)))
+        return Matrix(self.ctx, h)
+
+    def __del__(self):
+        if sys is None or sys.is_finalizing():
+            return
+        if getattr(self, "_h", None):
+            lib().spg_staged_free(self._h)
+            self._h = None
 
 
 def upload_device(ctx: Context, dimension: int, leaf_size: int, n_leaves: int, d_rows: int,

@@ -78,6 +78,7 @@ struct spg_context {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H of product chunks overlapping the GEMM
   cudaStream_t aux_stream = nullptr;   // second compute stream for chunked GEMMs
+  cudaStream_t h2d_stream = nullptr;   // staged uploads (next input while this product runs)
   cudaEvent_t ev[8] = {};
   std::mutex mu;
   int64_t launches = 0;   // own kernels launched (evidence counter)

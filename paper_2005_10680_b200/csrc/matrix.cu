@@ -278,7 +278,9 @@ __global__ void leaf_ptr_kernel(const double* payload, int64_t n, int64_t LL,
 }
 
 const double* const* leaf_table(spg_context* ctx, const spg_matrix* m) {
-  if (!m->payload || m->n_slots == 0) return nullptr;
+  // cached in the matrix, from its own context's pool: only on that context
+  // (another context's call may run concurrently with the owner's)
+  if (!m->payload || m->n_slots == 0 || m->ctx != ctx) return nullptr;
   auto* mm = const_cast<spg_matrix*>(m);  // cache: built once, read-only afterwards
   if (!mm->leaf_ptrs) {
     mm->leaf_ptrs = dev_alloc<const double*>(m->n_slots, ctx);
@@ -447,6 +449,7 @@ int spg_context_create(int device, spg_context** out) {
   SPG_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
   SPG_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   SPG_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  SPG_CUDA(cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking));
   for (auto& e : ctx->ev) SPG_CUDA(cudaEventCreate(&e));
   *out = ctx.release();
   SPG_API_END
@@ -464,6 +467,7 @@ int spg_context_destroy(spg_context* ctx) {
   cudaStreamDestroy(ctx->stream);
   cudaStreamDestroy(ctx->copy_stream);
   cudaStreamDestroy(ctx->aux_stream);
+  cudaStreamDestroy(ctx->h2d_stream);
   delete ctx;
   SPG_API_END
 }
@@ -518,6 +522,87 @@ int spg_matrix_upload(spg_context* ctx, int32_t dimension, int32_t leaf_size, in
   *out = matrix_from_device_leaves(ctx, dimension, leaf_size, n_leaves, rows.get(), cols.get(),
                                    d_payload);
   SPG_API_END
+}
+
+// ---- staged uploads: the copies run on the context's h2d stream, so the
+// next input streams in while the current product computes
+}  // extern "C"
+
+struct spg_staged {
+  spg_context* ctx = nullptr;
+  int32_t dimension = 0, leaf = 0;
+  int64_t n = 0;
+  spg::DevBuf<int32_t> rows, cols;
+  double* payload = nullptr;
+  cudaEvent_t done = nullptr;
+  ~spg_staged() {
+    if (payload) spg::dev_free(payload, ctx);
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+extern "C" {
+
+int spg_matrix_stage(spg_context* ctx, int32_t dimension, int32_t leaf_size, int64_t n_leaves,
+                     const int32_t* block_rows, const int32_t* block_cols, const double* payload,
+                     spg_staged** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  if (n_leaves < 0) fail(SPG_EINVAL, "negative leaf count");
+  if (n_leaves && (!block_rows || !block_cols || !payload)) fail(SPG_EINVAL, "null leaf arrays");
+  CtxGuard g(ctx);
+  int32_t padded, depth;
+  check_shape(dimension, leaf_size, &padded, &depth);
+  auto st = std::make_unique<spg_staged>();
+  st->ctx = ctx;
+  st->dimension = dimension;
+  st->leaf = leaf_size;
+  st->n = n_leaves;
+  const int64_t elems = static_cast<int64_t>(leaf_size) * leaf_size;
+  st->rows = DevBuf<int32_t>(std::max<int64_t>(n_leaves, 1), ctx);
+  st->cols = DevBuf<int32_t>(std::max<int64_t>(n_leaves, 1), ctx);
+  st->payload = dev_alloc<double>(std::max<int64_t>(n_leaves * elems, 1), ctx);
+  SPG_CUDA(cudaEventCreateWithFlags(&st->done, cudaEventDisableTiming));
+  // pool blocks are handed out in ctx->stream order: start after it
+  SPG_CUDA(cudaEventRecord(st->done, ctx->stream));
+  SPG_CUDA(cudaStreamWaitEvent(ctx->h2d_stream, st->done, 0));
+  if (n_leaves) {
+    SPG_CUDA(cudaMemcpyAsync(st->rows.get(), block_rows, n_leaves * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->h2d_stream));
+    SPG_CUDA(cudaMemcpyAsync(st->cols.get(), block_cols, n_leaves * sizeof(int32_t),
+                             cudaMemcpyHostToDevice, ctx->h2d_stream));
+    SPG_CUDA(cudaMemcpyAsync(st->payload, payload, n_leaves * elems * sizeof(double),
+                             cudaMemcpyHostToDevice, ctx->h2d_stream));
+  }
+  SPG_CUDA(cudaEventRecord(st->done, ctx->h2d_stream));
+  *out = st.release();
+  SPG_API_END
+}
+
+int spg_matrix_stage_finish(spg_staged* st, spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!st || !out) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  std::unique_ptr<spg_staged> own(st);
+  spg_context* ctx = st->ctx;
+  CtxGuard g(ctx);
+  SPG_CUDA(cudaStreamWaitEvent(ctx->stream, st->done, 0));
+  double* p = st->payload;
+  st->payload = nullptr;  // owned by the matrix from here on
+  *out = matrix_from_device_leaves(ctx, st->dimension, st->leaf, st->n, st->rows.get(),
+                                   st->cols.get(), p);
+  SPG_API_END
+}
+
+void spg_staged_free(spg_staged* st) {
+  if (!st) return;
+  try {
+    CtxGuard g(st->ctx);
+    SPG_CUDA(cudaEventSynchronize(st->done));
+    delete st;
+  } catch (...) {
+  }
 }
 
 int spg_matrix_upload_device(spg_context* ctx, int32_t dimension, int32_t leaf_size,

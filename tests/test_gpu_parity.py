@@ -213,3 +213,37 @@ def test_parity_audit_counts(ctx, port):
     tau = float(norms[0] * norms[0])  # the (0,0,0) leaf product itself
     ties, _ = nat.parity_audit(ctx, A, A, tau, 0)
     assert ties >= 1
+
+
+def test_staged_upload_equals_upload_and_overlaps_a_product(ctx):
+    """spg_matrix_stage / stage_finish: the same matrix as spg_matrix_upload
+    (bitwise), also when staged while a product is queued on the context."""
+    import torch
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    rows, cols, pay = nat.synth_chain_host(2048, 64, 40.0, 9, 1e-10)
+    h_rows = torch.from_numpy(rows).pin_memory()
+    h_cols = torch.from_numpy(cols).pin_memory()
+    h_pay = torch.from_numpy(np.ascontiguousarray(pay)).pin_memory()
+    A = nat.upload(ctx, 2048, 64, rows, cols, pay)
+    st = nat.Staged(ctx, 2048, 64, len(rows), h_rows.data_ptr(), h_cols.data_ptr(),
+                    h_pay.data_ptr())
+    S = st.finish()
+    for lvl in range(6):
+        assert bits_equal(S.level_norms(lvl), A.level_norms(lvl))
+    ra, ca, pa, na = A.download()
+    rs, cs, ps, ns = S.download()
+    assert np.array_equal(ra, rs) and np.array_equal(ca, cs) and bits_equal(pa, ps)
+    taus = log_grid(32)
+    C0, s0, b0 = nat.spamm_with_error_control(ctx, A, A, 1e-6, taus)
+    nxt = nat.Staged(ctx, 2048, 64, len(rows), h_rows.data_ptr(), h_cols.data_ptr(),
+                     h_pay.data_ptr())
+    C1, s1, b1 = nat.spamm_with_error_control(ctx, S, S, 1e-6, taus)  # runs while nxt copies
+    N = nxt.finish()
+    C2, s2, b2 = nat.spamm_with_error_control(ctx, N, N, 1e-6, taus)
+    for Ck, bk in ((C1, b1), (C2, b2)):
+        assert bits_equal(bk, b0)
+        assert bits_equal(Ck.download()[2], C0.download()[2])
+    abandoned = nat.Staged(ctx, 2048, 64, len(rows), h_rows.data_ptr(), h_cols.data_ptr(),
+                           h_pay.data_ptr())
+    del abandoned  # spg_staged_free waits for its copies
