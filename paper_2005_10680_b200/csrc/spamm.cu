@@ -261,8 +261,8 @@ void launch_tma64(spg_context* ctx, const double* A, const double* B, const int2
 
 int gemm_variant() {
   static const int v = [] {
-    const char* e = std::getenv("SPG_GEMM");  // developer switch: 2 = cp.async kernel
-    return e ? std::atoi(e) : 5;
+    const char* e = std::getenv("SPG_GEMM");  // developer switch (variants below)
+    return e ? std::atoi(e) : 4;
   }();
   return v;
 }
@@ -310,15 +310,25 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
       else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v32 == 6) launch_dmma<32, 32, 32, 16, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v32 == 7) launch_dmma<32, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v32 == 8) launch_dmma<32, 32, 16, 16, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       break;
     }
     case 64:
       launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       break;
-    case 128:
-      launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+    case 128: {
+      static const int v128 = [] {
+        const char* e = std::getenv("SPG_GEMM128");  // developer switch for the L=128 tiling
+        return e ? std::atoi(e) : 3;
+      }();
+      if (v128 == 2) launch_dmma<128, 16, 64, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else if (v128 == 3) launch_dmma<128, 32, 64, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
+      else launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab);
       break;
+    }
     default: {
       const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_out, int64_t(1) << 30));
       leaf_gemm_generic<<<grid, 256, 0, st>>>(A, B, pairs, out_offset, n_out, L, C, out_end,
