@@ -213,6 +213,12 @@ int spg_matrix_axpby(spg_context* ctx, double alpha, const spg_matrix* a, double
                      const spg_matrix* b, spg_matrix** out);
 /* QuadTreeMatrix::identity (quadtree.cpp:231-235). */
 int spg_matrix_identity(spg_context* ctx, int32_t dimension, int32_t leaf_size, spg_matrix** out);
+/* diag(d): leaves on the block diagonal holding d (host array of length n). */
+int spg_matrix_from_diagonal(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                             const double* diag, spg_matrix** out);
+/* Per row i (host arrays of length n, either may be NULL): the diagonal entry
+ * and sum_j |a_ij| (ascending j) -- Gershgorin data for spectral bounds. */
+int spg_matrix_rows(const spg_matrix* m, double* diag, double* abs_row_sums);
 
 /* ---- SP2 purification over the GPU product (purification.cpp:49-202;
  * SURVEY.md 8f row 2, BASELINE config 3) ----------------------------------- */

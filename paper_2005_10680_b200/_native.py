@@ -174,6 +174,8 @@ _SIGNATURES = {
                                    C.POINTER(_vp)]),
     "spg_matrix_stage_finish": (C.c_int, [_vp, C.POINTER(_vp)]),
     "spg_staged_free": (None, [_vp]),
+    "spg_matrix_from_diagonal": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.POINTER(_vp)]),
+    "spg_matrix_rows": (C.c_int, [_vp, _dp, _dp]),
     "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
                                              _dp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
     "spg_matrix_gather_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64, _vp]),
@@ -556,6 +558,23 @@ def axpby(ctx: Context, alpha: float, a: Matrix, beta: float = 0.0, b: Matrix | 
     _check(lib().spg_matrix_axpby(ctx.handle, alpha, a.handle, beta, b.handle if b else None,
                                   C.byref(h)))
     return Matrix(ctx, h)
+
+
+def from_diagonal(ctx: Context, diag, leaf: int) -> Matrix:
+    d = np.ascontiguousarray(diag, np.float64)
+    h = _vp()
+    _check(lib().spg_matrix_from_diagonal(ctx.handle, d.size, leaf, _ptr(d, C.c_double),
+                                          C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def row_data(m: Matrix):
+    """(diagonal, sum_j |a_ij|) per row, computed on the device."""
+    n = m.dimension
+    d = np.empty(n, np.float64)
+    a = np.empty(n, np.float64)
+    _check(lib().spg_matrix_rows(m.handle, _ptr(d, C.c_double), _ptr(a, C.c_double)))
+    return d, a
 
 
 def identity(ctx: Context, n: int, leaf: int) -> Matrix:

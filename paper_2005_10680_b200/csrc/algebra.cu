@@ -77,6 +77,31 @@ __global__ void axpby_blocks(const uint64_t* __restrict__ keys, int64_t n, doubl
   }
 }
 
+// per row i: the diagonal entry and sum_j |a_ij| in ascending j (deterministic)
+__global__ void row_scan_kernel(const int32_t* __restrict__ grid_slot, int32_t dimension,
+                                int32_t nb_logical, const double* __restrict__ payload, int L,
+                                double* __restrict__ diag, double* __restrict__ abs_sum) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= dimension) return;
+  const uint32_t br = static_cast<uint32_t>(i / L);
+  const int r = i % L;
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  double s = 0.0, dv = 0.0;
+  for (uint32_t bc = 0; bc < static_cast<uint32_t>(nb_logical); ++bc) {
+    const int32_t slot = grid_slot[morton2(br, bc)];
+    if (slot < 0) continue;
+    const double* blk = payload + static_cast<int64_t>(slot) * LL + r;
+    const int jn = min(L, dimension - static_cast<int>(bc) * L);
+    for (int j = 0; j < jn; ++j) {
+      const double v = blk[static_cast<int64_t>(j) * L];
+      s = __dadd_rn(s, fabs(v));
+      if (bc == br && j == r) dv = v;
+    }
+  }
+  if (diag) diag[i] = dv;
+  if (abs_sum) abs_sum[i] = s;
+}
+
 }  // namespace
 
 double trace_device(spg_context* ctx, const spg_matrix* m) {
@@ -157,7 +182,8 @@ spg_matrix* axpby_device(spg_context* ctx, double alpha, const spg_matrix* a, do
   return matrix_from_morton_blocks(ctx, a->dimension, a->leaf, n, out_keys, payload);
 }
 
-spg_matrix* identity_device(spg_context* ctx, int32_t dimension, int32_t leaf) {
+spg_matrix* diagonal_device(spg_context* ctx, int32_t dimension, int32_t leaf,
+                            const double* diag) {
   int32_t padded, depth;
   check_shape(dimension, leaf, &padded, &depth);
   const int32_t nb = (dimension + leaf - 1) / leaf;
@@ -167,7 +193,7 @@ spg_matrix* identity_device(spg_context* ctx, int32_t dimension, int32_t leaf) {
   for (int32_t i = 0; i < nb; ++i) {
     rows[i] = i;
     for (int32_t k = 0; k < leaf && i * leaf + k < dimension; ++k)
-      pay[i * LL + k + static_cast<int64_t>(k) * leaf] = 1.0;
+      pay[i * LL + k + static_cast<int64_t>(k) * leaf] = diag ? diag[i * leaf + k] : 1.0;
   }
   DevBuf<int32_t> d_rows(nb, ctx);
   double* d_pay = dev_alloc<double>(nb * LL, ctx);
@@ -176,6 +202,10 @@ spg_matrix* identity_device(spg_context* ctx, int32_t dimension, int32_t leaf) {
   SPG_CUDA(cudaMemcpyAsync(d_pay, pay.data(), nb * LL * sizeof(double), cudaMemcpyHostToDevice,
                            ctx->stream));
   return matrix_from_device_leaves(ctx, dimension, leaf, nb, d_rows.get(), d_rows.get(), d_pay);
+}
+
+spg_matrix* identity_device(spg_context* ctx, int32_t dimension, int32_t leaf) {
+  return diagonal_device(ctx, dimension, leaf, nullptr);
 }
 
 }  // namespace spg
@@ -207,6 +237,37 @@ int spg_matrix_axpby(spg_context* ctx, double alpha, const spg_matrix* a, double
   *out = nullptr;
   CtxGuard g(ctx);
   *out = axpby_device(ctx, alpha, a, beta, b);
+  SPG_API_END
+}
+
+int spg_matrix_from_diagonal(spg_context* ctx, int32_t dimension, int32_t leaf_size,
+                             const double* diag, spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out || !diag) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  CtxGuard g(ctx);
+  *out = diagonal_device(ctx, dimension, leaf_size, diag);
+  SPG_API_END
+}
+
+int spg_matrix_rows(const spg_matrix* m, double* diag, double* abs_row_sums) {
+  SPG_API_BEGIN
+  if (!m) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
+  spg_context* ctx = m->ctx;
+  CtxGuard g(ctx);
+  const int32_t n = m->dimension, nb = (n + m->leaf - 1) / m->leaf;
+  DevBuf<double> d(n, ctx), a(n, ctx);
+  row_scan_kernel<<<grid_for(n, 128), 128, 0, ctx->stream>>>(m->grid_slot, n, nb, m->payload,
+                                                             m->leaf, d.get(), a.get());
+  SPG_CHECK_LAUNCH(ctx);
+  if (diag)
+    SPG_CUDA(cudaMemcpyAsync(diag, d.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  if (abs_row_sums)
+    SPG_CUDA(cudaMemcpyAsync(abs_row_sums, a.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
   SPG_API_END
 }
 

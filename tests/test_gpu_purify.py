@@ -174,3 +174,22 @@ def test_against_reference_driver(ctx, ref, variant):
     rr, rc_, rp, _ = T.leaves()
     dr = nat.leaves_to_dense(256, 16, rr, rc_, rp)
     assert np.linalg.norm(D.to_dense() - dr) < 1e-9
+
+
+def test_row_data_and_diagonal_matrices(ctx):
+    """spg_matrix_rows (diagonal, sum_j |a_ij|) and spg_matrix_from_diagonal
+    against numpy, ragged last block included."""
+    from paper_2005_10680_b200 import _native as nat
+    rng = np.random.default_rng(4)
+    n, L = 333, 16
+    d = np.where(rng.uniform(size=(n, n)) < 0.3, rng.uniform(-1, 1, (n, n)), 0.0)
+    d[:, 50:70] = 0.0
+    A = nat.from_dense(ctx, d, L)
+    diag, rs = nat.row_data(A)
+    assert np.array_equal(diag, np.diag(d))
+    ref = np.array([sum(abs(x) for x in row) for row in d])  # ascending j, sequential
+    assert np.array_equal(rs, ref)
+    v = rng.uniform(-2, 2, n)
+    D = nat.from_diagonal(ctx, v, L)
+    assert np.array_equal(D.to_dense(), np.diag(v))
+    assert nat.trace(D) == pytest.approx(v.sum(), rel=1e-14)
