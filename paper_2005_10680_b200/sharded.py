@@ -211,11 +211,25 @@ class DistributedOperands:
             nat.ipc_close(self.ctx, ptr)
         self.opened = []
 
-    def controlled_product(self, delta: float, taus, fetch=None, panel_rows: int = 8):
-        """This rank's rows of spamm_with_error_control(A, B, delta, taus)."""
+    def controlled_product(self, delta: float, taus, fetch=None, panel_rows: int = 8,
+                           row_chunks: int = 1):
+        """This rank's rows of spamm_with_error_control(A, B, delta, taus).
+
+        row_chunks = 2^c (peer transport): the rank's block rows are
+        multiplied in 2^c consecutive sub-shards, one task list at a time, so
+        the task list (16 B per surviving product) never holds more than a
+        1/2^c share -- config 4's ~6e9 products per rank would not fit
+        otherwise.  B is read in place, so chunking moves no extra data.
+        Returns C as one matrix (row_chunks = 1) or the list of chunk
+        matrices in row order."""
         import numpy as np
         if not (delta > 0.0):
             raise ValueError("spamm_with_error_control: delta must be positive")
+        c = max(0, int(row_chunks).bit_length() - 1)
+        if row_chunks < 1 or (1 << c) != row_chunks:
+            raise ValueError("row_chunks must be a power of two")
+        if c and self.transport != "peer":
+            raise ValueError("row_chunks needs the peer transport (panels would be re-sent)")
         taus = np.ascontiguousarray(taus, np.float64)
         nat.tolerance_grid_check(taus)
         level = self.level
@@ -227,19 +241,31 @@ class DistributedOperands:
             bounds = nat.cse_finish(level, nat.top_norms(self.A_norms, level),
                                     nat.top_norms(self.B_norms, level), parts)
         tau, k = nat.select_tolerance(bounds, taus, delta)
-        plan = nat.Plan(self.ctx, self.A, self.B_norms, tau, level, self.rank,
-                        a_norms=self.A_norms)
+        pieces, stats = [], []
+        moved = 0
+        for sub in range(1 << c):
+            plan = nat.Plan(self.ctx, self.A, self.B_norms, tau, level + c,
+                            (self.rank << c) + sub, a_norms=self.A_norms)
+            if self.transport == "peer":
+                plan.run_table(self.bases, self.slot_owner, self.slot_local)
+            else:
+                moved += run_panels(self.ctx, plan,
+                                    panel_schedule(self.n, self.L, level, panel_rows), fetch,
+                                    self.L)
+            C, st = plan.finish()
+            plan.free()
+            pieces.append(C)
+            stats.append(st)
+        st = dict(stats[0])
+        for key in ("candidates", "survivors", "output_blocks", "flops", "ms_tasklist", "ms_gemm",
+                    "ms_finalize"):
+            st[key] = sum(x[key] for x in stats)
         if self.transport == "peer":
-            plan.run_table(self.bases, self.slot_owner, self.slot_local)
             mine = self.slot_owner == self.rank
-            moved = int((~mine).sum()) * self.L * self.L * 8  # upper bound: leaves read remotely
-        else:
-            moved = run_panels(self.ctx, plan,
-                               panel_schedule(self.n, self.L, level, panel_rows), fetch, self.L)
-        C, st = plan.finish()
-        plan.free()
-        return C, {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
-                   "spamm": st, "panel_bytes": moved}, bounds
+            moved = int((~mine).sum()) * self.L * self.L * 8  # leaves read remotely (distinct)
+        return (pieces[0] if c == 0 else pieces), \
+            {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
+             "spamm": st, "panel_bytes": moved}, bounds
 
 
 def controlled_product_distributed(ctx, A_local, B_local, delta: float, taus, level: int,

@@ -288,3 +288,36 @@ def test_two_ranks_gloo_distributed_driver(ctx, tmp_path, transport):
     key0 = np.lexsort((c, r))
     assert np.array_equal(rr[key], r[key0]) and np.array_equal(cc[key], c[key0])
     assert bits_equal(pp[key], p[key0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunks", [1, 2, 8])
+def test_peer_row_chunks_bitwise(ctx, chunks):
+    """DistributedOperands(transport="peer") on one rank with the rows split in
+    2^c task-list chunks: the chunk products, in row order, are the resident
+    product's blocks, bitwise."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    from paper_2005_10680_b200.sharded import DistributedOperands
+    n, L = 2048, 32
+    A = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 1, 1e-10)
+    B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10)
+    ops = DistributedOperands(ctx, A, B, 0, 0, lambda arrays: [arrays], transport="peer")
+    C, st, bounds = ops.controlled_product(1e-6, log_grid(32), row_chunks=chunks)
+    ops.close()
+    ref, sref, bref = nat.spamm_with_error_control(ctx, A, B, 1e-6, log_grid(32))
+    assert bits_equal(bounds, bref) and st["tau"] == sref["tau"]
+    assert st["spamm"]["survivors"] == sref["spamm"]["survivors"]
+    pieces = C if isinstance(C, list) else [C]
+    assert len(pieces) == chunks
+    got = [p.download() for p in pieces]
+    r = np.concatenate([g[0] for g in got])
+    c = np.concatenate([g[1] for g in got])
+    p = np.concatenate([g[2] for g in got])
+    r0, c0, p0, _ = ref.download()
+    k, k0 = np.lexsort((c, r)), np.lexsort((c0, r0))
+    assert np.array_equal(r[k], r0[k0]) and np.array_equal(c[k], c0[k0])
+    assert bits_equal(p[k], p0[k0])
+    with pytest.raises(ValueError):
+        ops2 = DistributedOperands(ctx, A, B, 0, 0, lambda arrays: [arrays])
+        ops2.controlled_product(1e-6, log_grid(32), fetch=lambda *a: None, row_chunks=2)
