@@ -374,6 +374,19 @@ def run_ours(args, dist):
     }
     if clk:
         out["clocks"] = clk
+    # K1 (leaf norms, block_norm) on A: the norm-table kernel's HBM roofline
+    # (8 L^2 bytes read per leaf; best of 3 timed passes)
+    norm_ms = min(A.norm_pass_ms() for _ in range(3))
+    norm_bytes = float(A.nnz_blocks) * w.leaf * w.leaf * 8  # non-null leaves (conservative)
+    out["norm_roofline"] = {"kernel": "leaf_norm_kernel (K1)", "bound": "hbm",
+                            "achieved": round(norm_bytes / (norm_ms / 1e3) / 1e9, 1),
+                            "peak": hbm, "unit": "GB/s",
+                            "frac": round(norm_bytes / (norm_ms / 1e3) / 1e9 / hbm, 4),
+                            "peak_source": hbm_src + " (a copy: read+write; this kernel only "
+                                                     "reads)",
+                            "frac_of_spec_7700": round(norm_bytes / (norm_ms / 1e3) / 1e9 / 7700.0,
+                                                       4),
+                            "ms": round(norm_ms, 3), "algorithmic": "8 L^2 B read per leaf"}
     if distributed:
         out["panel_bytes_per_step"] = int(st["panel_bytes"])
     if not split:  # SURVEY 8a parity audit: how close the decisions are to ties

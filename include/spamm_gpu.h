@@ -349,6 +349,9 @@ void spg_plan_free(spg_plan* plan);
  * of B's leaf count (slots of the norm-only B); replaces the panels. */
 int spg_plan_run_table(spg_plan* plan, int32_t n_owners, const double* const* owner_base,
                        const int32_t* slot_owner, const int32_t* slot_local, void* stream);
+/* One timed pass of the leaf-norm kernel (K1, block_norm) over every leaf
+ * of m (results discarded): *ms = device time.  For roofline reporting. */
+int spg_matrix_norm_pass(const spg_matrix* m, float* ms);
 /* Device address of a matrix's leaf payload (slot t at base + t * L*L). */
 int spg_matrix_payload(const spg_matrix* m, const double** base);
 /* Payload slot of every non-null leaf, in spg_matrix_download order. */

@@ -166,6 +166,7 @@ _SIGNATURES = {
     "spg_plan_free": (None, [_vp]),
     "spg_plan_run_table": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), _i32p, _i32p, _vp]),
     "spg_matrix_payload": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "spg_matrix_norm_pass": (C.c_int, [_vp, C.POINTER(C.c_float)]),
     "spg_matrix_payload_slots": (C.c_int, [_vp, _i32p]),
     "spg_ipc_export": (C.c_int, [_vp, C.c_char_p]),
     "spg_ipc_open": (C.c_int, [_vp, C.c_char_p, C.POINTER(_vp)]),
@@ -337,6 +338,12 @@ class Matrix:
         out = np.empty((n, n), np.float64)
         _check(lib().spg_matrix_to_dense(self._h, _ptr(out, C.c_double)))
         return out
+
+    def norm_pass_ms(self) -> float:
+        """Device time of one leaf-norm kernel pass over every leaf."""
+        ms = C.c_float(0)
+        _check(lib().spg_matrix_norm_pass(self._h, C.byref(ms)))
+        return ms.value
 
     def payload_ptr(self) -> int:
         p = _vp()

@@ -850,6 +850,25 @@ int spg_matrix_gather_rows(const spg_matrix* m, int32_t row_begin, int32_t row_e
 }
 
 
+int spg_matrix_norm_pass(const spg_matrix* m, float* ms) {
+  SPG_API_BEGIN
+  if (!m || !ms) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
+  spg_context* ctx = m->ctx;
+  CtxGuard g(ctx);
+  const int64_t n = m->n_slots;
+  DevBuf<double> norms(std::max<int64_t>(n, 1), ctx);
+  DevBuf<uint8_t> nz(std::max<int64_t>(n, 1), ctx);
+  const int32_t nb = (m->dimension + m->leaf - 1) / m->leaf;
+  SPG_CUDA(cudaEventRecord(ctx->ev[6], ctx->stream));
+  leaf_norms(ctx, m->payload, n, m->leaf, m->dimension, nb, nullptr, nullptr, norms.get(),
+             nz.get(), nullptr);
+  SPG_CUDA(cudaEventRecord(ctx->ev[7], ctx->stream));
+  SPG_CUDA(cudaEventSynchronize(ctx->ev[7]));
+  SPG_CUDA(cudaEventElapsedTime(ms, ctx->ev[6], ctx->ev[7]));
+  SPG_API_END
+}
+
 int spg_matrix_payload(const spg_matrix* m, const double** base) {
   SPG_API_BEGIN
   if (!m || !base) fail(SPG_EINVAL, "null argument");

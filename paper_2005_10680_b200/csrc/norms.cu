@@ -44,17 +44,26 @@ __global__ void __launch_bounds__(kNormWarps * 32)
     my_c = cols[base + lane];
   }
 
+  // Software-pipelined: the next chunk's 32 loads are in flight while this
+  // chunk's squares are summed; nonzero flags accumulate per lane and are
+  // OR-reduced once at the end (no per-element ballot).
   double sum = 0.0;
-  unsigned nz_mask = 0;  // bit j: leaf j has a nonzero entry
+  unsigned my_nz = 0;  // bit j: this lane saw a nonzero entry of leaf j
+  double cur[32];
+  auto load_chunk = [&](int64_t e0) {
+    const int cnt = (elems - e0 < 32) ? static_cast<int>(elems - e0) : 32;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      cur[j] = (j < nleaf && lane < cnt) ? __ldg(payload + (base + j) * elems + e0 + lane) : 0.0;
+  };
+  load_chunk(0);
   for (int64_t e0 = 0; e0 < elems; e0 += 32) {
     const int cnt = (elems - e0 < 32) ? static_cast<int>(elems - e0) : 32;
     const int64_t e = e0 + lane;
-#pragma unroll 8
+#pragma unroll
     for (int j = 0; j < 32; ++j) {
-      double v = 0.0;
-      if (j < nleaf && lane < cnt) v = __ldg(payload + (base + j) * elems + e);
-      const unsigned any = __ballot_sync(0xffffffffu, v != 0.0);
-      if (any) nz_mask |= (1u << j);
+      const double v = cur[j];
+      my_nz |= static_cast<unsigned>(v != 0.0) << j;
       if (kCheckPadding) {
         const int32_t r = __shfl_sync(0xffffffffu, my_r, j);
         const int32_t c = __shfl_sync(0xffffffffu, my_c, j);
@@ -68,12 +77,14 @@ __global__ void __launch_bounds__(kNormWarps * 32)
       sq[warp][j][lane] = __dmul_rn(v, v);
     }
     __syncwarp();
+    if (e0 + 32 < elems) load_chunk(e0 + 32);
     if (lane < nleaf) {
       const double* row = sq[warp][lane];
       for (int i = 0; i < cnt; ++i) sum = __dadd_rn(sum, row[i]);
     }
     __syncwarp();
   }
+  const unsigned nz_mask = __reduce_or_sync(0xffffffffu, my_nz);
   if (lane < nleaf) {
     norms[base + lane] = __dsqrt_rn(sum);
     nonzero[base + lane] = (nz_mask >> lane) & 1u;
