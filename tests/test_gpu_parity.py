@@ -247,3 +247,27 @@ def test_staged_upload_equals_upload_and_overlaps_a_product(ctx):
     abandoned = nat.Staged(ctx, 2048, 64, len(rows), h_rows.data_ptr(), h_cols.data_ptr(),
                            h_pay.data_ptr())
     del abandoned  # spg_staged_free waits for its copies
+
+
+def test_nan_entries_follow_the_reference(ctx, ref):
+    """A NaN entry makes its leaf norm NaN (non-null, block_norm): the sweep
+    treats the leaf's products as never skipped-error (NaN < tau is false at
+    every k), the skip test keeps them (!(NaN < tau)); bounds, survivors and
+    norms match the reference bit for bit."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import geometric_grid, log_grid
+    rng = np.random.default_rng(31)
+    n, L = 300, 8
+    d = _random_case(rng, n, L, 0.6, 30.0)
+    d[17, 40] = np.nan
+    d[250, 3] = np.nan
+    lv = nat.dense_to_leaves(d, L)
+    A = nat.upload(ctx, n, L, *lv)
+    tr = ref.build(n, L, *lv)
+    for lvl in range(tr.depth() + 1):
+        assert bits_equal(A.level_norms(lvl), tr.level_norms(lvl))
+    for taus in (log_grid(32, 1.0, 1e-8), geometric_grid(10.0, 0.8, 60)):
+        b = nat.cse(ctx, A, A, taus)
+        assert bits_equal(b, ref.cse(tr, tr, taus))
+        tau = float(taus[len(taus) // 2])
+        assert np.array_equal(nat.survivors(ctx, A, A, tau), ref.survivors(tr, tr, tau))
