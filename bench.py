@@ -62,9 +62,10 @@ def parse():
                    help="distributed: each rank holds only its block rows of A and B; B panels "
                         "are broadcast by their owners (SURVEY 8e, configs 4/5)")
     p.add_argument("--panel-rows", type=int, default=32)
-    p.add_argument("--transport", default="peer", choices=["peer", "broadcast"],
-                   help="distributed operands: B leaves read in place from the owners' memory "
-                        "(CUDA IPC / NVLink, one GEMM) or broadcast in panels")
+    p.add_argument("--transport", default="broadcast", choices=["peer", "broadcast"],
+                   help="distributed operands: B panels broadcast by their owners (each leaf "
+                        "crosses NVLink once per product) or read in place from the owners' "
+                        "memory by one GEMM (CUDA IPC / NVLink; every L2 miss crosses the link)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-rows", type=int, default=4,
