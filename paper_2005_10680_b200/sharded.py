@@ -215,11 +215,13 @@ class DistributedOperands:
                            row_chunks: int = 1):
         """This rank's rows of spamm_with_error_control(A, B, delta, taus).
 
-        row_chunks = 2^c (peer transport): the rank's block rows are
-        multiplied in 2^c consecutive sub-shards, one task list at a time, so
-        the task list (16 B per surviving product) never holds more than a
-        1/2^c share -- config 4's ~6e9 products per rank would not fit
-        otherwise.  B is read in place, so chunking moves no extra data.
+        row_chunks = 2^c: the rank's block rows are multiplied in 2^c
+        consecutive sub-shards, one task list at a time, so the task list (16 B
+        per surviving product) never holds more than a 1/2^c share -- config
+        4's ~6e9 products per rank would not fit otherwise.  With the
+        broadcast transport every chunk receives B again (2^c x B per product;
+        config 4 at c = 3: ~3 TB per rank, ~4 s over NVLink against ~130 s of
+        GEMM); the peer transport reads B in place either way.
         Returns C as one matrix (row_chunks = 1) or the list of chunk
         matrices in row order."""
         import numpy as np
@@ -228,8 +230,6 @@ class DistributedOperands:
         c = max(0, int(row_chunks).bit_length() - 1)
         if row_chunks < 1 or (1 << c) != row_chunks:
             raise ValueError("row_chunks must be a power of two")
-        if c and self.transport != "peer":
-            raise ValueError("row_chunks needs the peer transport (panels would be re-sent)")
         taus = np.ascontiguousarray(taus, np.float64)
         nat.tolerance_grid_check(taus)
         level = self.level

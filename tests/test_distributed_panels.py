@@ -319,5 +319,35 @@ def test_peer_row_chunks_bitwise(ctx, chunks):
     assert np.array_equal(r[k], r0[k0]) and np.array_equal(c[k], c0[k0])
     assert bits_equal(p[k], p0[k0])
     with pytest.raises(ValueError):
-        ops2 = DistributedOperands(ctx, A, B, 0, 0, lambda arrays: [arrays])
-        ops2.controlled_product(1e-6, log_grid(32), fetch=lambda *a: None, row_chunks=2)
+        ops.controlled_product(1e-6, log_grid(32), row_chunks=3)
+
+
+@pytest.mark.gpu
+def test_broadcast_row_chunks_bitwise(ctx):
+    """Broadcast transport with the rows in 4 task-list chunks (each chunk
+    receives the B panels again): the chunk products are the resident
+    product's blocks, bitwise."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    from paper_2005_10680_b200.sharded import DistributedOperands
+    n, L = 2048, 64
+    A = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 1, 1e-10)
+    B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10)
+    ops = DistributedOperands(ctx, A, B, 0, 0, lambda arrays: [arrays])
+
+    def fetch(r0, r1, owner, buf, count, stream):
+        nat.gather_rows(B, r0, r1, buf.data_ptr(), count, stream.cuda_stream)
+
+    pieces, st, bounds = ops.controlled_product(1e-6, log_grid(32), fetch, panel_rows=4,
+                                                row_chunks=4)
+    ref, sref, _ = nat.spamm_with_error_control(ctx, A, B, 1e-6, log_grid(32))
+    assert st["spamm"]["survivors"] == sref["spamm"]["survivors"]
+    got = [p.download() for p in pieces]
+    r = np.concatenate([g[0] for g in got])
+    c = np.concatenate([g[1] for g in got])
+    p = np.concatenate([g[2] for g in got])
+    r0, c0, p0, _ = ref.download()
+    k, k0 = np.lexsort((c, r)), np.lexsort((c0, r0))
+    assert np.array_equal(r[k], r0[k0]) and np.array_equal(c[k], c0[k0])
+    assert bits_equal(p[k], p0[k0])
+    assert st["panel_bytes"] == 4 * int(ops.B_norms.nnz_blocks) * L * L * 8
