@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
     leaf_gemm_dmma(const double* __restrict__ A, const double* __restrict__ B,
                    const int2* __restrict__ pairs, const int64_t* __restrict__ out_offset,
                    int64_t n_out, double* __restrict__ C, const int64_t* __restrict__ out_end,
-                   int accumulate, const double* const* __restrict__ btab) {
+                   int accumulate, const double* const* __restrict__ btab,
+                   const int32_t* __restrict__ order = nullptr) {
   using Cfg = DmmaGemmCfg<L, KC, WM, WN, NSTAGE>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
@@ -84,7 +85,8 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
   const int n0 = (warp / Cfg::WARPS_M) * WN;
   constexpr int64_t LL = static_cast<int64_t>(L) * L;
 
-  for (int64_t o = blockIdx.x; o < n_out; o += gridDim.x) {
+  for (int64_t ob = blockIdx.x; ob < n_out; ob += gridDim.x) {
+    const int64_t o = order ? order[ob] : ob;
     // products of block o: pairs[beg, end); a B-panel launch passes its own
     // end[] and continues the accumulator stored by the previous panel
     const int64_t beg = out_offset[o];
@@ -185,9 +187,11 @@ static __global__ void leaf_gemm_generic(const double* __restrict__ A, const dou
                                   const int2* __restrict__ pairs,
                                   const int64_t* __restrict__ out_offset, int64_t n_out, int L,
                                   double* __restrict__ C, const int64_t* __restrict__ out_end,
-                                  int accumulate, const double* const* __restrict__ btab) {
+                                  int accumulate, const double* const* __restrict__ btab,
+                                  const int32_t* __restrict__ order) {
   const int64_t LL = static_cast<int64_t>(L) * L;
-  for (int64_t o = blockIdx.x; o < n_out; o += gridDim.x) {
+  for (int64_t ob = blockIdx.x; ob < n_out; ob += gridDim.x) {
+    const int64_t o = order ? order[ob] : ob;
     const int64_t beg = out_offset[o], end = out_end ? out_end[o] : out_offset[o + 1];
     if (beg == end) continue;
     for (int64_t e = threadIdx.x; e < LL; e += blockDim.x) {
