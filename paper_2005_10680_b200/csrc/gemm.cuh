@@ -58,7 +58,8 @@ struct DmmaGemmCfg {
   static constexpr int TM = WM / 8;
   static constexpr int TN = WN / 8;
   static constexpr size_t kSmemBytes = sizeof(double) * NSTAGE * STAGE;
-  static_assert(kWarps == 1 || kWarps == 2 || kWarps == 4 || kWarps == 8, "1-8 warps per CTA");
+  static_assert(kWarps == 1 || kWarps == 2 || kWarps == 4 || kWarps == 8 || kWarps == 16,
+                "1-16 warps per CTA");
   static_assert(AS % 16 == 4 && BS % 16 == 4, "bank-conflict-free strides");
   static_assert(L % KC == 0 && KC % 4 == 0, "k chunking");
 };

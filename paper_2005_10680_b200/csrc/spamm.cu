@@ -328,6 +328,7 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
       }();
       if (v128 == 2) launch_dmma<128, 16, 64, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
       else if (v128 == 3) launch_dmma<128, 32, 64, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
+      else if (v128 == 4) launch_dmma<128, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
       else launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
       break;
     }
