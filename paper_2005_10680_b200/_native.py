@@ -12,9 +12,7 @@ SPG_EINVAL -> ValueError (std::invalid_argument), SPG_ERANGE -> IndexError
 from __future__ import annotations
 
 import ctypes as C
-import os
 import sys
-from dataclasses import dataclass
 from pathlib import Path
 
 import numpy as np
