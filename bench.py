@@ -216,13 +216,16 @@ def cpu_sample(kind, rows, cols, pay, w, taus, tau_star, sample_rows, threads):
     return flops / dt / 1e12, dt, flops, surv
 
 
-def traffic_from_profile():
-    p = ROOT / "profiles" / "ncu_summary.json"
+def ncu_entry(key):
+    """The ncu capture summarised for `key` in profiles/ncu_summary.json (or {})."""
     try:
-        d = json.loads(p.read_text())
-        return d["leaf_gemm_dmma"]["dram_bytes_per_launch"]
+        return json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get(key, {})
     except Exception:
-        return None
+        return {}
+
+
+def traffic_from_profile():
+    return ncu_entry("leaf_gemm_dmma").get("dram_bytes_per_launch")
 
 
 def run_ours(args, dist):
@@ -370,7 +373,12 @@ def run_ours(args, dist):
         "sweep_roofline": {"kernel": "cse (tile + reduce)", "bound": "hbm",
                            "achieved": round(sweep_gbs, 2), "peak": hbm, "unit": "GB/s",
                            "frac": round(sweep_gbs / hbm, 5), "peak_source": hbm_src,
-                           "algorithmic": "12 B per candidate leaf product (SURVEY 8d)"},
+                           "algorithmic": "12 B per candidate leaf product (SURVEY 8d)",
+                           # a tiled sweep is FP64-ALU bound -- the ncu capture
+                           # (profiles/) of its tile kernel, for the other side of the picture
+                           "ncu_tile_kernel": {k: ncu_entry("cse_tile_kernel").get(k) for k in (
+                               "duration", "dram_bytes_per_launch", "fp64_pipe_active_pct",
+                               "issue_active_pct")}},
         "gpu_launches": launches,
     }
     if clk:

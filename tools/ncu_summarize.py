@@ -67,9 +67,16 @@ def main(rep, out, key=None):
         summ = json.loads(summ_path.read_text()) if summ_path.exists() else {}
         rd = scale(*m["dram__bytes_read.sum"])
         wr = scale(*m["dram__bytes_write.sum"])
+        def pct(k):
+            return float(m[k][0]) if k in m else None
         summ[key] = {"report": Path(rep).name, "kernel": kname,
                      "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
-                     "duration": " ".join(m["gpu__time_duration.sum"])}
+                     "duration": " ".join(m["gpu__time_duration.sum"]),
+                     "fp64_pipe_active_pct":
+                         pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                     "dmma_pipe_active_pct": pct(
+                         "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active"),
+                     "issue_active_pct": pct("sm__throughput.avg.pct_of_peak_sustained_elapsed")}
         summ_path.write_text(json.dumps(summ, indent=1) + "\n")
 
 
