@@ -306,7 +306,7 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
     case 32: {
       static const int v32 = [] {
         const char* e = std::getenv("SPG_GEMM32");  // developer switch for the L=32 tiling
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 6;
       }();
       if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
       else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
