@@ -5,9 +5,9 @@
 // Truncation semantics, bit for bit: leaves ordered by (norm, row-major block
 // position) ascending; walking that order a leaf is removed while
 // sqrt(fl(s + fl(n*n))) < delta, with s accumulating fl(s + fl(n*n)) in the
-// same order.  The running sum is inherently sequential, so one thread walks
-// the sorted norms and stops at the first leaf that does not fit (the sort is
-// the parallel part).  Removed leaves become null; inner norms are rebuilt by
+// same order.  The running sum is inherently sequential: one thread runs its
+// add chain chunk by chunk while the block checks the stop test in parallel
+// (trunc_walk); the sort is the other parallel part.  Removed leaves become null; inner norms are rebuilt by
 // K2 (combine_child_norms), which equals the reference's make_inner on the
 // changed paths and its cached norms everywhere else.  The result shares the
 // input's leaf payload -- nothing is copied.
@@ -41,20 +41,60 @@ __global__ void trunc_gather_norms(const int64_t* __restrict__ index, int64_t n,
   norm_bits[t] = static_cast<uint64_t>(__double_as_longlong(leaf_level[keys[index[t]]]));
 }
 
-// the sequential greedy walk (one thread): removed count and sqrt(sum)
-__global__ void trunc_walk(const uint64_t* __restrict__ sorted_norm_bits, int64_t n, double delta,
-                           int64_t* __restrict__ count, double* __restrict__ removed) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double s = 0.0;
-  int64_t c = 0;
-  for (; c < n; ++c) {
-    const double v = __longlong_as_double(static_cast<long long>(sorted_norm_bits[c]));
-    const double t = __dadd_rn(s, __dmul_rn(v, v));
-    if (!(__dsqrt_rn(t) < delta)) break;
-    s = t;
+// The greedy walk.  The running sum is a sequential FP recurrence, but the
+// stop test is not part of it: s_c = fl(s_{c-1} + fl(n_c^2)) is the plain
+// prefix sum up to the first c with !(sqrt(s_c) < delta), and the removed
+// count is that c.  So one thread runs only the DADD chain for a chunk of
+// kWalkChunk leaves into shared memory, then the block tests the chunk's
+// prefix sums in parallel (correctly rounded sqrt, same comparison) and
+// stops at the first failure -- bit-identical to the one-leaf-at-a-time
+// loop, with the square root and the branch off the dependency chain.
+constexpr int kWalkChunk = 4096;
+
+__global__ void __launch_bounds__(256) trunc_walk(const uint64_t* __restrict__ sorted_norm_bits,
+                                                  int64_t n, double delta,
+                                                  int64_t* __restrict__ count,
+                                                  double* __restrict__ removed) {
+  __shared__ double pref[kWalkChunk];
+  __shared__ int first_fail;
+  __shared__ double carry;  // prefix sum before the chunk
+  if (threadIdx.x == 0) carry = 0.0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += kWalkChunk) {
+    const int len = static_cast<int>(n - base < kWalkChunk ? n - base : kWalkChunk);
+    // squares in parallel (coalesced loads), then the add chain alone
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+      const double v = __longlong_as_double(static_cast<long long>(sorted_norm_bits[base + i]));
+      pref[i] = __dmul_rn(v, v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = carry;
+      first_fail = len;
+      for (int i = 0; i < len; ++i) {
+        s = __dadd_rn(s, pref[i]);
+        pref[i] = s;
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < len; i += blockDim.x)
+      if (!(__dsqrt_rn(pref[i]) < delta)) atomicMin(&first_fail, i);
+    __syncthreads();
+    const int f = first_fail;
+    if (f < len) {
+      if (threadIdx.x == 0) {
+        *count = base + f;
+        *removed = __dsqrt_rn(f > 0 ? pref[f - 1] : carry);
+      }
+      return;
+    }
+    if (threadIdx.x == 0) carry = pref[len - 1];
+    __syncthreads();
   }
-  *count = c;
-  *removed = __dsqrt_rn(s);
+  if (threadIdx.x == 0) {
+    *count = n;
+    *removed = __dsqrt_rn(carry);
+  }
 }
 
 __global__ void trunc_slot_flags(const uint64_t* __restrict__ keys,
@@ -119,7 +159,7 @@ spg_matrix* truncate_device(spg_context* ctx, const spg_matrix* x, double delta,
                                              idx_pos.get(), idx_sorted.get(), n, 0, 64,
                                              ctx->stream));
     ctx->lib_calls++;
-    trunc_walk<<<1, 32, 0, ctx->stream>>>(nbits_sorted.get(), n, delta, d_count.get(),
+    trunc_walk<<<1, 256, 0, ctx->stream>>>(nbits_sorted.get(), n, delta, d_count.get(),
                                           d_removed.get());
     SPG_CHECK_LAUNCH(ctx);
     trunc_slot_flags<<<grid_for(n, 256), 256, 0, ctx->stream>>>(x->keys, x->slots, n, leaf_level,
