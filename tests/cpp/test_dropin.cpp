@@ -18,6 +18,7 @@
 #include "spamm/error_control.hpp"
 #include "spamm/execution.hpp"
 #include "spamm/multiply.hpp"
+#include "spamm/oracle.hpp"
 #include "spamm/purification.hpp"
 #include "spamm/quadtree.hpp"
 
@@ -509,6 +510,120 @@ TEST(purify_sp2, "sp2 selection, budget, and convergence to the projector") {
   spamm::PurificationConfig bad;
   bad.occupation = 0;
   CHECK_THROWS_AS(spamm::purify(diag_matrix({1.0, 0.0}, 2), bad), std::invalid_argument);
+}
+
+static const spamm::Variant kVariants[] = {spamm::Variant::truncmul, spamm::Variant::spamm,
+                                           spamm::Variant::hybrid};
+
+TEST(purify_idempotent_start, "an idempotent start with the right trace converges at once") {
+  const auto proj = diag_matrix({1.0, 1.0, 0.0, 0.0}, 4);
+  for (auto v : kVariants) {
+    spamm::PurificationConfig cfg;
+    cfg.variant = v;
+    cfg.occupation = 2;
+    cfg.epsilon = 1e-6;
+    const auto r = spamm::purify(proj, cfg);
+    CHECK(r.converged && r.iterations == 0);
+    CHECK(bitwise_equal(r.density.to_dense(), proj.to_dense()));
+    CHECK(!r.log.empty() && r.log.back().status == "converged");
+  }
+}
+
+TEST(purify_per_iteration, "each logged iteration meets its own tolerance") {
+  for (auto v : kVariants) {
+    spamm::PurificationConfig cfg;
+    cfg.variant = v;
+    cfg.occupation = 2;
+    cfg.epsilon = 1e-6;
+    const auto r = spamm::purify(diag_matrix({0.9, 0.8, 0.2, 0.1}, 4), cfg);
+    for (const auto& rec : r.log)
+      if (rec.status != "converged") CHECK(rec.status == "ok" && rec.realized_error < rec.tolerance);
+  }
+}
+
+TEST(purify_zero_budget, "a zero budget makes every variant exact and identical") {
+  spamm::oracle::DecayModelSpec spec;
+  spec.dimension = 48;
+  spec.alpha = 0.6;
+  spec.seed = 5;
+  const DenseMatrix f = spamm::oracle::generate_decay_matrix(spec);
+  const auto x0 = spamm::initial_transform(QuadTreeMatrix::from_dense(f, 16), {0.0, 2.0});
+  std::vector<DenseMatrix> dens;
+  std::vector<int> its;
+  std::vector<std::vector<double>> tr;
+  for (auto v : kVariants) {
+    spamm::PurificationConfig cfg;
+    cfg.variant = v;
+    cfg.occupation = 12;
+    cfg.epsilon = 1e-9;
+    cfg.budget = [](double, int n) {
+      spamm::ErrorBudget b;
+      b.deltas.assign(static_cast<size_t>(n), 0.0);
+      return b;
+    };
+    const auto r = spamm::purify(x0, cfg);
+    CHECK(r.converged);
+    dens.push_back(r.density.to_dense());
+    its.push_back(r.iterations);
+    std::vector<double> t;
+    for (const auto& rec : r.log) t.push_back(rec.trace);
+    tr.push_back(t);
+  }
+  for (int k = 1; k < 3; ++k) {
+    CHECK(its[k] == its[0]);
+    CHECK(bitwise_equal(dens[k], dens[0]));
+    CHECK(tr[k] == tr[0]);
+  }
+}
+
+TEST(purify_vs_eigensolver, "decay-model purification matches the eigensolver projector") {
+  spamm::oracle::DecayModelSpec spec;
+  spec.dimension = 128;
+  spec.alpha = 0.55;
+  spec.seed = 9;
+  const DenseMatrix f = spamm::oracle::generate_decay_matrix(spec);
+  const DenseMatrix proj = spamm::oracle::density_matrix_oracle(f, 32);
+  const auto x0 = spamm::initial_transform(QuadTreeMatrix::from_dense(f, 32), {0.0, 2.0});
+  for (auto v : kVariants) {
+    spamm::PurificationConfig cfg;
+    cfg.variant = v;
+    cfg.occupation = 32;
+    cfg.epsilon = 1e-5;
+    const auto r = spamm::purify(x0, cfg);
+    CHECK(r.converged);
+    CHECK(diff_frob(r.density.to_dense(), proj) < 1e-5);
+    CHECK(std::abs(r.density.trace() - 32.0) < 1e-3);
+    for (const auto& rec : r.log)
+      if (rec.status != "converged") CHECK(rec.realized_error < rec.tolerance);
+  }
+}
+
+TEST(purify_cap_and_validation, "iteration cap reports non-convergence; bad configs throw") {
+  spamm::oracle::DecayModelSpec spec;
+  spec.dimension = 64;
+  spec.alpha = 0.5;
+  spec.seed = 21;
+  const auto x0 = spamm::initial_transform(
+      QuadTreeMatrix::from_dense(spamm::oracle::generate_decay_matrix(spec), 32), {0.0, 2.0});
+  spamm::PurificationConfig cfg;
+  cfg.variant = spamm::Variant::hybrid;
+  cfg.occupation = 16;
+  cfg.epsilon = 1e-6;
+  cfg.max_iterations = 2;
+  const auto r = spamm::purify(x0, cfg);
+  CHECK(!r.converged && r.iterations == 2 && r.log.size() >= 2);
+  const auto small = diag_matrix({1.0, 0.0}, 2);
+  spamm::PurificationConfig bad;
+  bad.occupation = 2;  // == dimension
+  CHECK_THROWS_AS(spamm::purify(small, bad), std::invalid_argument);
+  bad.occupation = 1;
+  bad.epsilon = 0.0;
+  CHECK_THROWS_AS(spamm::purify(small, bad), std::invalid_argument);
+  bad.epsilon = 1e-6;
+  bad.max_iterations = 0;
+  CHECK_THROWS_AS(spamm::purify(small, bad), std::invalid_argument);
+  CHECK_THROWS_AS(spamm::ErrorBudget::geometric(0.0, 10), std::invalid_argument);
+  CHECK_THROWS_AS(spamm::ErrorBudget::geometric(1e-5, 0), std::invalid_argument);
 }
 
 int main() {
