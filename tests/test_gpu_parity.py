@@ -162,6 +162,28 @@ def test_sweep_kernel_variants_every_grid_size(ctx, port, n_taus):
     assert bits_equal(nat.cse(ctx, A, B, wide), port.cse(ta, tb, wide))
 
 
+@pytest.mark.parametrize("n_taus", [32, 64, 128])
+def test_sweep_wide_breakpoint_ranges(ctx, port, n_taus):
+    """Leaf blocks whose norms spread over ten decades inside every quadtree
+    node: a level d-1 node's live tau range then spans most of the grid, a
+    half-tile holds more items than the tile kernel's flat array and is
+    evaluated one level d-2 group at a time -- still bit-identical."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    rng = np.random.default_rng(900 + n_taus)
+    n, L = 512, 8
+    nb = n // L
+    scale = np.repeat(np.repeat(10.0 ** rng.uniform(-10, 0, (nb, nb)), L, 0), L, 1)
+    da = rng.uniform(-1, 1, (n, n)) * scale
+    db = rng.uniform(-1, 1, (n, n)) * scale.T
+    la, lb = nat.dense_to_leaves(da, L), nat.dense_to_leaves(db, L)
+    A, B = nat.upload(ctx, n, L, *la), nat.upload(ctx, n, L, *lb)
+    ta, tb = port.build(n, L, *la), port.build(n, L, *lb)
+    taus = log_grid(n_taus, 1.0, 1e-14)
+    assert bits_equal(nat.cse(ctx, A, B, taus), port.cse(ta, tb, taus))
+    assert bits_equal(nat.cse(ctx, A, A, taus), port.cse(ta, ta, taus))
+
+
 def test_run_to_run_determinism(ctx):
     """SPEC determinism (test_multiply.cpp:140-156 analogue): repeated calls are
     bitwise identical."""
