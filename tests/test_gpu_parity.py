@@ -184,6 +184,32 @@ def test_sweep_wide_breakpoint_ranges(ctx, port, n_taus):
     assert bits_equal(nat.cse(ctx, A, A, taus), port.cse(ta, ta, taus))
 
 
+@pytest.mark.parametrize("env", [{"SPG_CSE_LISTS": "1"}, {"SPG_CSE_FOLD": "2"},
+                                 {"SPG_CSE_FOLD": "2", "SPG_CSE_LISTS": "1"},
+                                 {"SPG_CSE_FOLD": "0"}, {"SPG_CSE": "6"}])
+def test_sweep_paths_in_subprocesses(port, env):
+    """Every sweep path (pair lists instead of dense enumeration, level s-1
+    folded into the tile CTAs or not, the v6 kernel) gives the oracle's bounds
+    bit for bit; the path is fixed per process, so each runs in a child."""
+    import os
+    import subprocess
+    import sys as _sys
+    from pathlib import Path
+    from paper_2005_10680_b200 import _native as nat
+    here = Path(__file__).resolve().parent
+    _sys.path.insert(0, str(here))
+    import sweep_paths_case as spc
+    out = subprocess.run([_sys.executable, str(here / "sweep_paths_case.py")],
+                         env={**os.environ, **env}, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    got = dict(line.split() for line in out.stdout.strip().splitlines())
+    for name, n, L, da, db, taus in spc.cases():
+        ta = port.build(n, L, *nat.dense_to_leaves(da, L))
+        tb = port.build(n, L, *nat.dense_to_leaves(db, L))
+        want = port.cse(ta, tb, taus).view(np.uint64).tobytes().hex()
+        assert got[name] == want, (env, name)
+
+
 def test_run_to_run_determinism(ctx):
     """SPEC determinism (test_multiply.cpp:140-156 analogue): repeated calls are
     bitwise identical."""
