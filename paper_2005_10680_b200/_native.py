@@ -12,13 +12,16 @@ SPG_EINVAL -> ValueError (std::invalid_argument), SPG_ERANGE -> IndexError
 from __future__ import annotations
 
 import ctypes as C
+import os
 import sys
 from pathlib import Path
 
 import numpy as np
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
-LIB_PATH = LIB_DIR / "libspamm_gpu.so"
+# SPG_LIB: developer override for A/B runs of compile-time variants
+# (tools/build_variant.py); the default is the in-tree library
+LIB_PATH = Path(os.environ["SPG_LIB"]) if os.environ.get("SPG_LIB") else LIB_DIR / "libspamm_gpu.so"
 
 SPG_OK, SPG_EINVAL, SPG_ERANGE, SPG_ENOMEM, SPG_ECUDA, SPG_ENCCL, SPG_EINTERNAL = range(7)
 
