@@ -401,30 +401,39 @@ Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
 // Morton order; only which CTA computes which block changes.  Concurrent CTAs
 // then share the A row panel A(i, :) (16 MB on cfg2: L2-resident), which cut
 // DRAM traffic and measured +1.5 % over Morton order on cfg2 (35.4 vs 34.9).
+// strip_log > 0: strips of 2^strip_log block rows, column-major inside a
+// strip, so the CTAs in flight also share each B leaf B(k, j) between the
+// strip's rows.
 __global__ void order_keys_kernel(const uint64_t* __restrict__ mkeys, int64_t n, int64_t chunk,
-                                  uint64_t* __restrict__ skeys, int32_t* __restrict__ idx) {
+                                  int strip_log, uint64_t* __restrict__ skeys,
+                                  int32_t* __restrict__ idx) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const uint64_t r = morton_row(mkeys[t]), c = morton_col(mkeys[t]);
-  skeys[t] = (static_cast<uint64_t>(t / chunk) << 48) | (r << 24) | c;
+  const uint64_t rs = r >> strip_log, ri = r & ((uint64_t(1) << strip_log) - 1);
+  skeys[t] = (static_cast<uint64_t>(t / chunk) << 48) | (rs << 30) | (c << 15) | ri;
   idx[t] = static_cast<int32_t>(t % chunk);
 }
 
-bool block_order_enabled() {
+// developer switch SPG_ORDER: 0 = Morton CTA order, 1 = row-major (default),
+// 2 + s = strips of 2^s block rows
+int block_order_mode() {
   static const int v = [] {
-    const char* e = std::getenv("SPG_ORDER");  // developer switch: 0 = Morton CTA order
+    const char* e = std::getenv("SPG_ORDER");
     return e ? std::atoi(e) : 1;
   }();
-  return v != 0;
+  return v;
 }
+bool block_order_enabled() { return block_order_mode() != 0; }
 
 DevBuf<int32_t> make_block_order(spg_context* ctx, const uint64_t* mkeys, int64_t n,
                                  int64_t chunk) {
   if (n < 2 || !block_order_enabled()) return DevBuf<int32_t>();
   DevBuf<uint64_t> k1(n, ctx), k2(n, ctx);
   DevBuf<int32_t> i1(n, ctx), i2(n, ctx);
-  order_keys_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(mkeys, n, chunk, k1.get(),
-                                                               i1.get());
+  const int strip_log = block_order_mode() >= 2 ? block_order_mode() - 2 : 0;
+  order_keys_kernel<<<grid_for(n, 256), 256, 0, ctx->stream>>>(mkeys, n, chunk, strip_log,
+                                                               k1.get(), i1.get());
   SPG_CHECK_LAUNCH(ctx);
   size_t bytes = 0;
   SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k1.get(), k2.get(), i1.get(), i2.get(),
