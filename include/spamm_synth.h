@@ -55,6 +55,17 @@ int spg_synth_cluster_device_rows(spg_context* ctx, int32_t n, int32_t leaf_size
                                   double density, uint64_t site_seed, uint64_t value_seed,
                                   double drop, int32_t row_begin, int32_t row_end,
                                   spg_matrix** out);
+/* The cluster generator's global scale (largest absolute row sum), and the
+ * row-range generator with that scale passed in: generating many row panels
+ * of one matrix (e.g. B streamed panel by panel) then skips the O(n^2) row
+ * sums per call.  With scale = spg_synth_cluster_scale(...) the output is
+ * bit-identical to spg_synth_cluster_device_rows. */
+int spg_synth_cluster_scale(spg_context* ctx, int32_t n, double ell, double density,
+                            uint64_t site_seed, uint64_t value_seed, double* scale);
+int spg_synth_cluster_device_rows_scaled(spg_context* ctx, int32_t n, int32_t leaf_size,
+                                         double ell, double density, uint64_t site_seed,
+                                         uint64_t value_seed, double drop, double scale,
+                                         int32_t row_begin, int32_t row_end, spg_matrix** out);
 
 #ifdef __cplusplus
 }

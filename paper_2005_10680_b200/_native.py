@@ -186,6 +186,12 @@ _SIGNATURES = {
     "spg_synth_cluster_device_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double,
                                                 C.c_double, C.c_uint64, C.c_uint64, C.c_double,
                                                 C.c_int32, C.c_int32, C.POINTER(_vp)]),
+    "spg_synth_cluster_scale": (C.c_int, [_vp, C.c_int32, C.c_double, C.c_double, C.c_uint64,
+                                          C.c_uint64, _dp]),
+    "spg_synth_cluster_device_rows_scaled": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_double,
+                                                       C.c_double, C.c_uint64, C.c_uint64,
+                                                       C.c_double, C.c_double, C.c_int32,
+                                                       C.c_int32, C.POINTER(_vp)]),
     "spg_synth_chain_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double,
                                        C.c_int64, _i32p, _i32p, _dp, _i64p]),
     "spg_synth_cluster_host": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double,
@@ -871,6 +877,26 @@ def synth_cluster_device_rows(ctx: Context, n: int, leaf: int, ell: float, densi
     h = _vp()
     _check(lib().spg_synth_cluster_device_rows(ctx.handle, n, leaf, ell, density, site_seed,
                                                value_seed, drop, row_begin, row_end, C.byref(h)))
+    return Matrix(ctx, h)
+
+
+def synth_cluster_scale(ctx: Context, n: int, ell: float, density: float, site_seed: int,
+                        value_seed: int) -> float:
+    """The cluster generator's global scale (largest absolute row sum)."""
+    out = C.c_double()
+    _check(lib().spg_synth_cluster_scale(ctx.handle, n, ell, density, site_seed, value_seed,
+                                         C.byref(out)))
+    return out.value
+
+
+def synth_cluster_device_rows_scaled(ctx: Context, n: int, leaf: int, ell: float, density: float,
+                                     site_seed: int, value_seed: int, drop: float, scale: float,
+                                     row_begin: int, row_end: int) -> Matrix:
+    """synth_cluster_device_rows with the scale passed in (no O(n^2) row sums)."""
+    h = _vp()
+    _check(lib().spg_synth_cluster_device_rows_scaled(ctx.handle, n, leaf, ell, density,
+                                                      site_seed, value_seed, drop, scale,
+                                                      row_begin, row_end, C.byref(h)))
     return Matrix(ctx, h)
 
 

@@ -244,6 +244,65 @@ spg_matrix* device_blocks_to_matrix(spg_context* ctx, int32_t n, int32_t L,
 }  // namespace
 }  // namespace spg
 
+namespace spg {
+namespace {
+// The cluster generator's sites and (if scale_in < 0) its global scale, the
+// largest absolute row sum, on the device.
+void cluster_setup(spg_context* ctx, int32_t n, double ell, double density, uint64_t site_seed,
+                   uint64_t value_seed, double scale_in, spg::DevBuf<double>* dsites,
+                   spg::DevBuf<double>* scale) {
+  using namespace spg;
+  if (n % 4 != 0) fail(SPG_EINVAL, "cluster dimension must be a multiple of 4");
+  if (!(ell > 0.0) || !(density > 0.0)) fail(SPG_EINVAL, "ell and density must be positive");
+  const std::vector<double> sites = cluster_sites(n / 4, density, site_seed, nullptr);
+  *dsites = DevBuf<double>(sites.size(), ctx);
+  SPG_CUDA(cudaMemcpyAsync(dsites->get(), sites.data(), sites.size() * sizeof(double),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  *scale = DevBuf<double>(1, ctx);
+  if (scale_in >= 0.0) {
+    SPG_CUDA(cudaMemcpyAsync(scale->get(), &scale_in, sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));  // scale_in is a host local
+    return;
+  }
+  DevBuf<double> rowsum(n, ctx);
+  cluster_rowsum_kernel<<<grid_for(int64_t(n) * 32, 256), 256, 0, ctx->stream>>>(
+      dsites->get(), n, ell, mix64(value_seed), rowsum.get());
+  SPG_CHECK_LAUNCH(ctx);
+  max_kernel<<<1, 256, 0, ctx->stream>>>(rowsum.get(), n, scale->get());
+  SPG_CHECK_LAUNCH(ctx);
+}
+
+spg_matrix* cluster_rows(spg_context* ctx, int32_t n, int32_t L, double ell, double density,
+                         uint64_t site_seed, uint64_t value_seed, double drop, double scale_in,
+                         int32_t row_begin, int32_t row_end) {
+  using namespace spg;
+  int32_t padded, depth;
+  check_shape(n, L, &padded, &depth);
+  if (row_begin < 0 || row_end < row_begin || row_end > (n + L - 1) / L)
+    fail(SPG_EINVAL, "synth: bad block row range");
+  DevBuf<double> dsites, scale;
+  cluster_setup(ctx, n, ell, density, site_seed, value_seed, scale_in, &dsites, &scale);
+  const uint64_t sm = mix64(value_seed);
+  const int32_t nb = (n + L - 1) / L;
+  const std::vector<uint64_t> hkeys = morton_blocks(nb, depth, row_begin, row_end);
+  const int64_t nblk = static_cast<int64_t>(hkeys.size());
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx);
+  SPG_CUDA(cudaMemcpyAsync(dkeys.get(), hkeys.data(), nblk * sizeof(uint64_t),
+                           cudaMemcpyHostToDevice, ctx->stream));
+  double* payload = dev_alloc<double>(std::max<int64_t>(nblk * LL, 1), ctx);
+  if (nblk) {
+    cluster_blocks_kernel<<<static_cast<unsigned>(std::min<int64_t>(nblk, 1 << 20)), 256, 0,
+                            ctx->stream>>>(dkeys.get(), nblk, dsites.get(), n, L, ell, sm,
+                                           scale.get(), drop, payload);
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  return device_blocks_to_matrix(ctx, n, L, hkeys, payload, dkeys);
+}
+}  // namespace
+}  // namespace spg
+
 using namespace spg;
 
 extern "C" {
@@ -358,39 +417,36 @@ int spg_synth_cluster_device_rows(spg_context* ctx, int32_t n, int32_t L, double
   SPG_API_BEGIN
   if (!ctx || !out) fail(SPG_EINVAL, "null argument");
   *out = nullptr;
-  if (n % 4 != 0) fail(SPG_EINVAL, "cluster dimension must be a multiple of 4");
-  if (!(ell > 0.0) || !(density > 0.0)) fail(SPG_EINVAL, "ell and density must be positive");
-  int32_t padded, depth;
-  check_shape(n, L, &padded, &depth);
-  if (row_begin < 0 || row_end < row_begin || row_end > (n + L - 1) / L)
-    fail(SPG_EINVAL, "synth: bad block row range");
   CtxGuard g(ctx);
-  const std::vector<double> sites = cluster_sites(n / 4, density, site_seed, nullptr);
-  DevBuf<double> dsites(sites.size(), ctx);
-  SPG_CUDA(cudaMemcpyAsync(dsites.get(), sites.data(), sites.size() * sizeof(double),
-                           cudaMemcpyHostToDevice, ctx->stream));
-  const uint64_t sm = mix64(value_seed);
-  DevBuf<double> rowsum(n, ctx), scale(1, ctx);
-  cluster_rowsum_kernel<<<grid_for(int64_t(n) * 32, 256), 256, 0, ctx->stream>>>(
-      dsites.get(), n, ell, sm, rowsum.get());
-  SPG_CHECK_LAUNCH(ctx);
-  max_kernel<<<1, 256, 0, ctx->stream>>>(rowsum.get(), n, scale.get());
-  SPG_CHECK_LAUNCH(ctx);
-  const int32_t nb = (n + L - 1) / L;
-  const std::vector<uint64_t> hkeys = morton_blocks(nb, depth, row_begin, row_end);
-  const int64_t nblk = static_cast<int64_t>(hkeys.size());
-  const int64_t LL = static_cast<int64_t>(L) * L;
-  DevBuf<uint64_t> dkeys(std::max<int64_t>(nblk, 1), ctx);
-  SPG_CUDA(cudaMemcpyAsync(dkeys.get(), hkeys.data(), nblk * sizeof(uint64_t),
-                           cudaMemcpyHostToDevice, ctx->stream));
-  double* payload = dev_alloc<double>(std::max<int64_t>(nblk * LL, 1), ctx);
-  if (nblk) {
-    cluster_blocks_kernel<<<static_cast<unsigned>(std::min<int64_t>(nblk, 1 << 20)), 256, 0,
-                            ctx->stream>>>(dkeys.get(), nblk, dsites.get(), n, L, ell, sm,
-                                           scale.get(), drop, payload);
-    SPG_CHECK_LAUNCH(ctx);
-  }
-  *out = device_blocks_to_matrix(ctx, n, L, hkeys, payload, dkeys);
+  *out = cluster_rows(ctx, n, L, ell, density, site_seed, value_seed, drop, -1.0, row_begin,
+                      row_end);
+  SPG_API_END
+}
+
+int spg_synth_cluster_scale(spg_context* ctx, int32_t n, double ell, double density,
+                            uint64_t site_seed, uint64_t value_seed, double* scale) {
+  SPG_API_BEGIN
+  if (!ctx || !scale) fail(SPG_EINVAL, "null argument");
+  CtxGuard g(ctx);
+  DevBuf<double> dsites, dscale;
+  cluster_setup(ctx, n, ell, density, site_seed, value_seed, -1.0, &dsites, &dscale);
+  SPG_CUDA(cudaMemcpyAsync(scale, dscale.get(), sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  SPG_API_END
+}
+
+int spg_synth_cluster_device_rows_scaled(spg_context* ctx, int32_t n, int32_t L, double ell,
+                                         double density, uint64_t site_seed, uint64_t value_seed,
+                                         double drop, double scale, int32_t row_begin,
+                                         int32_t row_end, spg_matrix** out) {
+  SPG_API_BEGIN
+  if (!ctx || !out) fail(SPG_EINVAL, "null argument");
+  *out = nullptr;
+  if (!(scale >= 0.0)) fail(SPG_EINVAL, "synth: scale must be non-negative");
+  CtxGuard g(ctx);
+  *out = cluster_rows(ctx, n, L, ell, density, site_seed, value_seed, drop, scale, row_begin,
+                      row_end);
   SPG_API_END
 }
 

@@ -351,3 +351,20 @@ def test_broadcast_row_chunks_bitwise(ctx):
     assert np.array_equal(r[k], r0[k0]) and np.array_equal(c[k], c0[k0])
     assert bits_equal(p[k], p0[k0])
     assert st["panel_bytes"] == 4 * int(ops.B_norms.nnz_blocks) * L * L * 8
+
+
+@pytest.mark.gpu
+def test_scaled_row_generator_is_bit_identical(ctx):
+    """spg_synth_cluster_device_rows_scaled with spg_synth_cluster_scale's
+    value reproduces spg_synth_cluster_device_rows bit for bit (the panel
+    generator of tools/cfg4_shard.py)."""
+    from paper_2005_10680_b200 import _native as nat
+    n, L = 4096, 64
+    scale = nat.synth_cluster_scale(ctx, n, 3.0, 0.1, 2005, 7)
+    for lo, hi in ((0, 16), (16, 40), (40, 64)):
+        a = nat.synth_cluster_device_rows(ctx, n, L, 3.0, 0.1, 2005, 7, 1e-10, lo, hi)
+        b = nat.synth_cluster_device_rows_scaled(ctx, n, L, 3.0, 0.1, 2005, 7, 1e-10, scale, lo, hi)
+        ra, ca, pa, na = a.download()
+        rb, cb, pb, nb_ = b.download()
+        assert np.array_equal(ra, rb) and np.array_equal(ca, cb)
+        assert bits_equal(pa, pb) and bits_equal(na, nb_)
