@@ -186,10 +186,13 @@ def test_sweep_wide_breakpoint_ranges(ctx, port, n_taus):
 
 @pytest.mark.parametrize("env", [{"SPG_CSE_LISTS": "1"}, {"SPG_CSE_FOLD": "2"},
                                  {"SPG_CSE_FOLD": "2", "SPG_CSE_LISTS": "1"},
-                                 {"SPG_CSE_FOLD": "0"}, {"SPG_CSE": "6"}])
+                                 {"SPG_CSE_FOLD": "0"}, {"SPG_CSE": "6"},
+                                 {"SPG_CSE_SYNC": "1", "SPG_CSE_LISTS": "1"},
+                                 {"SPG_CSE_SYNC": "1", "SPG_CSE_LISTS": "1", "SPG_CSE": "6"}])
 def test_sweep_paths_in_subprocesses(port, env):
     """Every sweep path (pair lists instead of dense enumeration, level s-1
-    folded into the tile CTAs or not, the v6 kernel) gives the oracle's bounds
+    folded into the tile CTAs or not, the v6 kernel, the host-synchronised
+    list path) gives the oracle's bounds
     bit for bit; the path is fixed per process, so each runs in a child."""
     import os
     import subprocess
