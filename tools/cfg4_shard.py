@@ -1,9 +1,10 @@
-"""BASELINE config 4 at full size: one shard of the 8-GPU run, on one B200.
+"""BASELINE configs 4 and 5 at full size: one shard of the 8-GPU run, on one B200.
 
 Config 4 (N = 262144, L = 64, 3-D cluster with ell = 4 A, A and B with
-independent value seeds, 64 log-spaced tau, delta = 1e-6) is sharded by
-output block row over 8 GPUs.  This runs everything rank
-`rank` of those 8 would do, on one GPU:
+independent value seeds, 64 log-spaced tau, delta = 1e-6) and config 5 (the
+config-4 form at N = 131072, L in {32, 64, 128}, delta in {1e-8, 1e-6, 1e-4},
+128 tau) are sharded by output block row over 8 GPUs.  This
+runs everything rank `rank` of those 8 would do, on one GPU:
   * the leaf-norm tables of every shard's A and B rows, each generated on the
     device shard by shard (what the all-gather of the tables delivers), and
     the global norm-only matrices built from them;
@@ -14,17 +15,21 @@ output block row over 8 GPUs.  This runs everything rank
     where on 8 GPUs the owner would broadcast them.
 A's rows stay resident (the rank's own shard).  The single-GPU sweep of the
 whole problem runs too, and its bounds must equal the sharded ones bit for bit.
+One JSON line per delta.
 
-    python tools/cfg4_shard.py [N] [rank] [ranks] [panel_rows] [row_chunks] [tau_lo]
+    python tools/cfg4_shard.py                       # config 4, delta 1e-6, grid [1e-12, 1e-2]
+    python tools/cfg4_shard.py --tau-lo 1e-16        # grid extended so delta = 1e-6 skips
+    python tools/cfg4_shard.py --config 5 --leaf 32  # config 5, one leaf size, all three deltas
 
-tau_lo: smallest candidate (default 1e-12, the config-1 range); at delta = 1e-6
-no tau of [1e-12, 1e-2] meets the bound on config 4 (exact fallback, tau = 0),
-so the grid can be extended downwards as for config 5 (tools/leaf_sweep.py).
+At delta = 1e-6 no tau of [1e-12, 1e-2] meets the bound on config 4 (exact
+fallback, tau = 0), so the grid can be extended downwards as for config 5
+(tools/leaf_sweep.py uses [1e-14, 1e-2]).
 """
+import argparse
 import json
-import sys
 import time
 
+import sys
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import numpy as np  # noqa: E402
 
@@ -33,21 +38,38 @@ from paper_2005_10680_b200.inputs import log_grid  # noqa: E402
 from paper_2005_10680_b200.sharded import (leaf_table, merge_tables, panel_schedule,  # noqa: E402
                                            run_panels)
 
-N = int(sys.argv[1]) if len(sys.argv) > 1 else 262144
-rank = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-ranks = int(sys.argv[3]) if len(sys.argv) > 3 else 8
-panel_rows = int(sys.argv[4]) if len(sys.argv) > 4 else 128
-row_chunks = int(sys.argv[5]) if len(sys.argv) > 5 else 8
-tau_lo = float(sys.argv[6]) if len(sys.argv) > 6 else 1e-12
-L, ELL, DENS, SITE, SEED_A, SEED_B, DROP = 64, 4.0, 0.1, 2005, 10680, 10681, 1e-10
-DELTA, NT = 1e-6, 64
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4, choices=[4, 5])
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--leaf", type=int, default=64)
+ap.add_argument("--rank", type=int, default=0)
+ap.add_argument("--ranks", type=int, default=8)
+ap.add_argument("--panel-rows", type=int, default=None)
+ap.add_argument("--row-chunks", type=int, default=8)
+ap.add_argument("--tau-lo", type=float, default=None)
+ap.add_argument("--deltas", default=None)
+args = ap.parse_args()
+cfg5 = args.config == 5
+N = args.n or (131072 if cfg5 else 262144)
+L = args.leaf
+NT = 128 if cfg5 else 64
+tau_lo = args.tau_lo or (1e-14 if cfg5 else 1e-12)
+deltas = [float(x) for x in (args.deltas or ("1e-8,1e-6,1e-4" if cfg5 else "1e-6")).split(",")]
+# panels of ~24 GB of dense leaves: every panel GEMM launch pays a per-block
+# accumulator reload, which weighs more the fewer products a block has per
+# panel (config 5, L = 64, delta = 1e-4: 22.7 TFLOP/s with 128-row panels,
+# 28.4 with 512-row panels)
+panel_rows = args.panel_rows or max(8, (24 << 30) // (N * L * 8))
+rank, ranks, row_chunks = args.rank, args.ranks, args.row_chunks
+ELL, DENS, SITE, SEED_A, SEED_B, DROP = 4.0, 0.1, 2005, 10680, 10681, 1e-10
 level = ranks.bit_length() - 1
 c = row_chunks.bit_length() - 1
 assert (1 << level) == ranks and (1 << c) == row_chunks
 
 ctx = nat.Context(0)
-out = {"workload": f"cfg4-cluster3d-N{N}-L{L}-ell{ELL}", "rank": rank, "ranks": ranks,
-       "n_taus": NT, "delta": DELTA, "panel_rows": panel_rows, "row_chunks": row_chunks}
+base = {"workload": f"cfg{args.config}-cluster3d-N{N}-L{L}-ell{ELL}", "rank": rank,
+        "ranks": ranks, "n_taus": NT, "tau_grid": [1e-2, tau_lo], "panel_rows": panel_rows,
+        "row_chunks": row_chunks}
 t0 = time.perf_counter()
 sA = nat.synth_cluster_scale(ctx, N, ELL, DENS, SITE, SEED_A)
 sB = nat.synth_cluster_scale(ctx, N, ELL, DENS, SITE, SEED_B)
@@ -69,17 +91,16 @@ ta, tb = merge_tables(tabA), merge_tables(tabB)
 A_norms = nat.from_leaf_norms(ctx, N, L, *ta)
 B_norms = nat.from_leaf_norms(ctx, N, L, *tb)
 ctx.synchronize()
-out["tables_s"] = round(time.perf_counter() - t0, 2)
-out["leaves_A"], out["leaves_B"] = int(len(ta[0])), int(len(tb[0]))
-out["leaves_A_rank"] = int(A_local.nnz_blocks)
+base["tables_s"] = round(time.perf_counter() - t0, 2)
+base["leaves_A"], base["leaves_B"] = int(len(ta[0])), int(len(tb[0]))
+base["leaves_A_rank"] = int(A_local.nnz_blocks)
 
 taus = log_grid(NT, 1e-2, tau_lo)
-out["tau_grid"] = [1e-2, tau_lo]
 ctx.synchronize()
 t1 = time.perf_counter()
 mine = nat.cse_shard(ctx, A_norms, B_norms, taus, level, rank)
 ctx.synchronize()
-out["sweep_shard_ms"] = round(1e3 * (time.perf_counter() - t1), 3)
+base["sweep_shard_ms"] = round(1e3 * (time.perf_counter() - t1), 3)
 parts = np.stack([mine if g == rank else nat.cse_shard(ctx, A_norms, B_norms, taus, level, g)
                   for g in range(ranks)])
 bounds = nat.cse_finish(level, nat.top_norms(A_norms, level), nat.top_norms(B_norms, level), parts)
@@ -87,15 +108,10 @@ ctx.synchronize()
 t2 = time.perf_counter()
 full = nat.cse(ctx, A_norms, B_norms, taus)
 ctx.synchronize()
-out["sweep_one_gpu_ms"] = round(1e3 * (time.perf_counter() - t2), 3)
-out["sharded_bounds_equal_one_gpu"] = bool(np.array_equal(full.view(np.uint64),
-                                                          bounds.view(np.uint64)))
-tau, k = nat.select_tolerance(bounds, taus, DELTA)
-out["tau"], out["tau_index"] = tau, k
-out["bound"] = float(bounds[k]) if k >= 0 else 0.0
-out["bound_at_smallest_tau"] = float(bounds[-1])
-
-LL = L * L
+base["sweep_one_gpu_ms"] = round(1e3 * (time.perf_counter() - t2), 3)
+base["sharded_bounds_equal_one_gpu"] = bool(np.array_equal(full.view(np.uint64),
+                                                           bounds.view(np.uint64)))
+base["bound_at_smallest_tau"] = float(bounds[-1])
 
 
 def fetch(r0, r1, owner, buf, count, stream):
@@ -108,25 +124,27 @@ def fetch(r0, r1, owner, buf, count, stream):
 
 
 sched = panel_schedule(N, L, 0, panel_rows)
-tot = {"candidates": 0, "survivors": 0, "flops": 0.0, "ms_gemm": 0.0, "ms_tasklist": 0.0,
-       "ms_finalize": 0.0, "output_blocks": 0}
-t3 = time.perf_counter()
-for sub in range(row_chunks):
-    plan = nat.Plan(ctx, A_local, B_norms, tau, level + c, (rank << c) + sub, a_norms=A_norms)
-    run_panels(ctx, plan, sched, fetch, L)
-    C, st = plan.finish()
-    plan.free()
-    for key in tot:
-        tot[key] += st[key]
-    print(json.dumps({"sub": sub, "survivors": st["survivors"], "ms_gemm": round(st["ms_gemm"], 1),
-                      "tflops": round(st["flops"] / st["ms_gemm"] / 1e9, 2) if st["ms_gemm"] else 0}),
-          flush=True)
-    C.free()
-ctx.synchronize()
-out["product_wall_s"] = round(time.perf_counter() - t3, 2)
-out.update({k2: (round(v, 1) if isinstance(v, float) else v) for k2, v in tot.items()})
-out["skipped_fraction"] = round(1 - tot["survivors"] / max(tot["candidates"], 1), 4)
-out["gemm_tflops"] = round(tot["flops"] / tot["ms_gemm"] / 1e9, 2)
-out["step_tflops_excl_panel_generation"] = round(
-    tot["flops"] / (tot["ms_gemm"] + tot["ms_tasklist"] + tot["ms_finalize"]) / 1e9, 2)
-print(json.dumps(out), flush=True)
+for delta in deltas:
+    out = dict(base)
+    out["delta"] = delta
+    tau, k = nat.select_tolerance(bounds, taus, delta)
+    out["tau"], out["tau_index"] = tau, k
+    out["bound"] = float(bounds[k]) if k >= 0 else 0.0
+    tot = {"candidates": 0, "survivors": 0, "flops": 0.0, "ms_gemm": 0.0, "ms_tasklist": 0.0,
+           "ms_finalize": 0.0, "output_blocks": 0}
+    t3 = time.perf_counter()
+    for sub in range(row_chunks):
+        plan = nat.Plan(ctx, A_local, B_norms, tau, level + c, (rank << c) + sub, a_norms=A_norms)
+        run_panels(ctx, plan, sched, fetch, L)
+        C, st = plan.finish()
+        plan.free()
+        for key in tot:
+            tot[key] += st[key]
+        C.free()
+    ctx.synchronize()
+    out["product_wall_s"] = round(time.perf_counter() - t3, 2)
+    out.update({k2: (round(v, 1) if isinstance(v, float) else v) for k2, v in tot.items()})
+    out["skipped_fraction"] = round(1 - tot["survivors"] / max(tot["candidates"], 1), 4)
+    out["gemm_tflops"] = round(tot["flops"] / tot["ms_gemm"] / 1e9, 2) if tot["ms_gemm"] else 0.0
+    out["sweep_shard_eff_gbs"] = round(12 * tot["candidates"] / (out["sweep_shard_ms"] / 1e3) / 1e9, 1)
+    print(json.dumps(out), flush=True)
