@@ -663,12 +663,19 @@ struct spg_plan {
   spg_spamm_stats stats{};
   cudaEvent_t ev[2] = {};
   cudaEvent_t t_first = nullptr, t_last = nullptr;  // GEMM phase: first panel .. finish
+  // per panel launch: (start, stop) around its kernels; ms_gemm = their sum
+  // (the phase span above also holds the waits for the panels themselves)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> panel_ev;
   bool started = false;
   ~spg_plan() {
     for (auto& x : ev)
       if (x) cudaEventDestroy(x);
     if (t_first) cudaEventDestroy(t_first);
     if (t_last) cudaEventDestroy(t_last);
+    for (auto& pe : panel_ev) {
+      cudaEventDestroy(pe.first);
+      cudaEventDestroy(pe.second);
+    }
   }
 };
 
@@ -742,6 +749,11 @@ void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_pan
   }
   const int L = b->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
+  std::pair<cudaEvent_t, cudaEvent_t> pe{};
+  SPG_CUDA(cudaEventCreate(&pe.first));
+  SPG_CUDA(cudaEventCreate(&pe.second));
+  plan->panel_ev.push_back(pe);
+  SPG_CUDA(cudaEventRecord(pe.first, ctx->stream));
   panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
       plan->pl.keys.get(), plan->pl.out_offset.get(), n_out, plan->pl.kbits,
       static_cast<uint32_t>(r0), static_cast<uint32_t>(r1), plan->beg.get(), plan->end.get());
@@ -752,6 +764,7 @@ void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_pan
   SPG_CHECK_LAUNCH(ctx);
   run_gemm(ctx, L, plan->a->payload, nullptr, plan->pl.pairs.get(), plan->beg.get(), n_out,
            plan->c.get(), ctx->stream, plan->end.get(), 1, plan->btab.get(), plan->order.get());
+  SPG_CUDA(cudaEventRecord(pe.second, ctx->stream));
 }
 
 // Every product at once, B leaf t read from btab[t] (one GEMM launch; the
@@ -797,8 +810,17 @@ spg_matrix* plan_finish(spg_plan* plan) {
   SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
   SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   SPG_CUDA(cudaEventElapsedTime(&plan->stats.ms_finalize, ctx->ev[4], ctx->ev[5]));
-  if (plan->started)
+  if (!plan->panel_ev.empty()) {  // panels: the sum of the panel launches' kernel time
+    float sum = 0.0f;
+    for (auto& pe : plan->panel_ev) {
+      float ms = 0.0f;
+      SPG_CUDA(cudaEventElapsedTime(&ms, pe.first, pe.second));
+      sum += ms;
+    }
+    plan->stats.ms_gemm = sum;
+  } else if (plan->started) {  // one table-addressed launch
     SPG_CUDA(cudaEventElapsedTime(&plan->stats.ms_gemm, plan->t_first, plan->t_last));
+  }
   return c;
 }
 
