@@ -412,4 +412,128 @@ __global__ void __launch_bounds__(TmaGemmCfg<NSTAGE>::kThreads, (NSTAGE <= 3) ? 
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// L = 32 super-block GEMM: one CTA per 2x2 group of output blocks
+// (rows 2I, 2I+1 x cols 2J, 2J+1), warp s = 2 ri + cj owning block
+// (2I+ri, 2J+cj) as a 32x32 tile (16 DMMA per 8 fragment loads).  Each
+// pipeline stage holds, for one k, the A leaves A(2I+ri, k) and B leaves
+// B(k, 2J+cj) any of the four blocks needs (entry mask bit s = product
+// (2I+ri, k, 2J+cj) survives), so a stage feeds up to four products: the
+// operand bytes per flop of an L = 64 product.  Every block still sees its
+// products in ascending k, each as the same 8 DMMA k-steps as in
+// leaf_gemm_dmma<32, ...>, so C~ is bitwise that kernel's.
+// ---------------------------------------------------------------------------
+struct SuperEntry {
+  int32_t a0, a1, b0, b1;  // A slots of rows 2I, 2I+1 at k; B slots of cols 2J, 2J+1
+};
+
+__global__ void __launch_bounds__(128, 3)
+    leaf_gemm_super32(const double* __restrict__ A, const double* const* __restrict__ btab,
+                      const SuperEntry* __restrict__ ent, const uint32_t* __restrict__ emask,
+                      const int64_t* __restrict__ sb_offset, const int32_t* __restrict__ sb_out,
+                      int64_t n_sb, double* __restrict__ C, const int32_t* __restrict__ order) {
+  constexpr int L = 32, S = 36;  // leaf, padded stride (== 4 mod 16)
+  constexpr int TILE = L * S;
+  constexpr int STAGE = 4 * TILE;  // A row 0, A row 1, B col 0, B col 1
+  constexpr int64_t LL = L * L;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3, pg = perm8(g);
+  const int ri = warp >> 1, cj = warp & 1;
+
+  for (int64_t sbi = blockIdx.x; sbi < n_sb; sbi += gridDim.x) {
+    const int64_t sb = order ? order[sbi] : sbi;
+    const int64_t beg = sb_offset[sb];
+    const int64_t n = sb_offset[sb + 1] - beg;
+
+    auto load_stage = [&](const SuperEntry& en, uint32_t m, int stage) {
+      double* st = smem + stage * STAGE;
+      // tile q: 0 = A row 2I, 1 = A row 2I+1, 2 = B col 2J, 3 = B col 2J+1
+      const bool need[4] = {(m & 3u) != 0, (m & 12u) != 0, (m & 5u) != 0, (m & 10u) != 0};
+      const double* src[4] = {A + static_cast<int64_t>(en.a0) * LL,
+                              A + static_cast<int64_t>(en.a1) * LL, btab[need[2] ? en.b0 : 0],
+                              btab[need[3] ? en.b1 : 0]};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!need[q]) continue;  // uniform per CTA
+        double* dst = st + q * TILE;
+#pragma unroll
+        for (int p = tid; p < L * L / 2; p += 128) {
+          // A: column kk of the leaf (L rows) -> dst[kk * S + row];
+          // B: column j of the leaf (L k-entries) -> dst[j * S + kk]; same copy
+          const int c = p / (L / 2), off = (p % (L / 2)) * 2;
+          cp_async16(dst + c * S + off, src[q] + c * L + off);
+        }
+      }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    // entries are fetched one step ahead, so their global latency hides
+    // behind a compute step (as pr_next in leaf_gemm_dmma)
+    SuperEntry en_next{};
+    uint32_t m_cur = 0, m_next = 0;
+    if (n > 0) {
+      m_cur = emask[beg];
+      load_stage(ent[beg], m_cur, 0);
+    }
+    cp_async_commit();
+    if (n > 1) {
+      en_next = ent[beg + 1];
+      m_next = emask[beg + 1];
+    }
+    for (int64_t step = 0; step < n; ++step) {
+      cp_async_wait<0>();
+      __syncthreads();
+      if (step + 1 < n) load_stage(en_next, m_next, static_cast<int>((step + 1) & 1));
+      cp_async_commit();
+      const uint32_t m_step = m_cur;
+      m_cur = m_next;
+      if (step + 2 < n) {
+        en_next = ent[beg + step + 2];
+        m_next = emask[beg + step + 2];
+      }
+      if ((m_step >> warp) & 1u) {
+        const double* st = smem + static_cast<int>(step & 1) * STAGE;
+        const double* As = st + ri * TILE;
+        const double* Bs = st + (2 + cj) * TILE;
+#pragma unroll
+        for (int ks = 0; ks < L / 4; ++ks) {
+          double a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = As[(4 * ks + t) * S + 8 * i + pg];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) b[j] = Bs[(8 * j + pg) * S + 4 * ks + t];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_884(acc[i][j], a[i], b[j]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    const int32_t o = sb_out[4 * sb + warp];
+    if (o >= 0) {
+      double* Cblk = C + static_cast<int64_t>(o) * LL;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int row = 8 * i + pg;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int col = 8 * j + perm8(2 * t + e);
+            Cblk[static_cast<int64_t>(col) * L + row] = acc[i][j][e];
+          }
+        }
+    }
+  }
+}
+
 }  // namespace spg

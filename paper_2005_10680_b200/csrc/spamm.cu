@@ -344,6 +344,76 @@ void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const i
 // Task list grouped by output block: C block o = Morton key out_keys[o] sums
 // the products pairs[out_offset[o], out_offset[o+1]) (k ascending); with
 // keep_keys the sorted (Morton(i,j) << depth | k) keys stay for B panels.
+// ---- L = 32 super-block task list (leaf_gemm_super32): survivors re-keyed
+// (super block, k, sub block), sorted; one entry per (super block, k).
+__global__ void super_keys(const uint64_t* __restrict__ keys, int64_t n, int kbits,
+                           uint64_t* __restrict__ key2, int64_t* __restrict__ val) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint64_t m = keys[t] >> kbits, k = keys[t] & ((uint64_t(1) << kbits) - 1);
+  key2[t] = ((m >> 2) << (kbits + 2)) | (k << 2) | (m & 3u);
+  val[t] = t;
+}
+
+__global__ void super_heads(const uint64_t* __restrict__ key2, int64_t n,
+                            int64_t* __restrict__ head) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  head[t] = (t == 0 || (key2[t] >> 2) != (key2[t - 1] >> 2)) ? 1 : 0;
+}
+
+// eidx: inclusive scan of the heads (entry of survivor t' = eidx - 1)
+__global__ void super_fill(const uint64_t* __restrict__ key2, const int64_t* __restrict__ val,
+                           const int64_t* __restrict__ eidx, int64_t n, int kbits,
+                           const int2* __restrict__ pairs, SuperEntry* __restrict__ ent,
+                           uint32_t* __restrict__ emask, uint64_t* __restrict__ ekey) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int64_t e = eidx[t] - 1;
+  const uint32_t sub = static_cast<uint32_t>(key2[t] & 3u);
+  const int2 pr = pairs[val[t]];
+  // the A slot of row ri (and the B slot of column cj) at this k is the same
+  // leaf for every sub block that shares it: concurrent writes agree
+  if (sub >> 1) ent[e].a1 = pr.x;
+  else ent[e].a0 = pr.x;
+  if (sub & 1u) ent[e].b1 = pr.y;
+  else ent[e].b0 = pr.y;
+  atomicOr(&emask[e], 1u << sub);
+  if (t == 0 || (key2[t] >> 2) != (key2[t - 1] >> 2)) ekey[e] = key2[t] >> (kbits + 2);
+}
+
+__global__ void super_sb_heads(const uint64_t* __restrict__ ekey, int64_t n_ent,
+                               uint8_t* __restrict__ flag) {
+  const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= n_ent) return;
+  flag[e] = (e == 0 || ekey[e] != ekey[e - 1]) ? 1 : 0;
+}
+
+__global__ void super_sb_finish(const uint64_t* __restrict__ ekey, const int64_t* __restrict__ heads,
+                                int64_t n_sb, int64_t n_ent, int64_t* __restrict__ sb_offset,
+                                uint64_t* __restrict__ sb_keys) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b > n_sb) return;
+  sb_offset[b] = b < n_sb ? heads[b] : n_ent;
+  if (b < n_sb) sb_keys[b] = ekey[heads[b]];
+}
+
+// output block o -> (super block, sub block) slot of sb_out
+__global__ void super_out(const uint64_t* __restrict__ out_keys, int64_t n_out,
+                          const uint64_t* __restrict__ sb_keys, int64_t n_sb,
+                          int32_t* __restrict__ sb_out) {
+  const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o >= n_out) return;
+  const uint64_t sup = out_keys[o] >> 2;
+  int64_t lo = 0, hi = n_sb;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sb_keys[mid] < sup) lo = mid + 1;
+    else hi = mid;
+  }
+  sb_out[4 * lo + static_cast<int64_t>(out_keys[o] & 3u)] = static_cast<int32_t>(o);
+}
+
 struct Plan {
   int64_t n_surv = 0, n_out = 0;
   int kbits = 0;
@@ -443,6 +513,100 @@ DevBuf<int32_t> make_block_order(spg_context* ctx, const uint64_t* mkeys, int64_
                                            i2.get(), n, 0, 64, ctx->stream));
   ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
   return i2;
+}
+
+// L = 32 resident product through leaf_gemm_super32 (the default; another
+// SPG_GEMM32 value selects a per-block tiling): the (super block, k) entry
+// list from the sorted survivor keys, then one CTA per 2x2 super block.
+// Config-5-style L = 32 product (tools/profile_leaf.py 32): 29.1 -> 32.3
+// TFLOP/s, C~ bitwise unchanged.
+bool super32_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPG_GEMM32");
+    return !e || std::atoi(e) == 9;
+  }();
+  return on;
+}
+
+void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,
+                 const double* const* btab, double* C) {
+  const int64_t n = pl.n_surv;
+  if (n == 0) return;
+  const int kbits = pl.kbits;
+  DevBuf<uint64_t> k2(n, ctx), k2s(n, ctx);
+  DevBuf<int64_t> v(n, ctx), vs(n, ctx);
+  super_keys<<<grid_for(n, 256), 256, 0, ctx->stream>>>(pl.keys.get(), n, kbits, k2.get(),
+                                                         v.get());
+  SPG_CHECK_LAUNCH(ctx);
+  size_t bytes = 0;
+  const int end_bit = 2 * depth + kbits;
+  SPG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, k2.get(), k2s.get(), v.get(), vs.get(),
+                                           n, 0, end_bit, ctx->stream));
+  {
+    DevBuf<uint8_t> tmp(bytes, ctx);
+    SPG_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, k2.get(), k2s.get(), v.get(),
+                                             vs.get(), n, 0, end_bit, ctx->stream));
+  }
+  k2.reset();
+  v.reset();
+  DevBuf<int64_t> head(n, ctx), eidx(n, ctx);
+  super_heads<<<grid_for(n, 256), 256, 0, ctx->stream>>>(k2s.get(), n, head.get());
+  SPG_CHECK_LAUNCH(ctx);
+  bytes = 0;
+  SPG_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, head.get(), eidx.get(), n, ctx->stream));
+  {
+    DevBuf<uint8_t> tmp(bytes, ctx);
+    SPG_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), bytes, head.get(), eidx.get(), n,
+                                           ctx->stream));
+  }
+  const int64_t n_ent = copy_scalar_to_host_i64(ctx, eidx.get() + n - 1);
+  DevBuf<SuperEntry> ent(n_ent, ctx);
+  DevBuf<uint32_t> emask(n_ent, ctx);
+  DevBuf<uint64_t> ekey(n_ent, ctx);
+  SPG_CUDA(cudaMemsetAsync(ent.get(), 0, n_ent * sizeof(SuperEntry), ctx->stream));
+  SPG_CUDA(cudaMemsetAsync(emask.get(), 0, n_ent * sizeof(uint32_t), ctx->stream));
+  super_fill<<<grid_for(n, 256), 256, 0, ctx->stream>>>(k2s.get(), vs.get(), eidx.get(), n, kbits,
+                                                         pl.pairs.get(), ent.get(), emask.get(),
+                                                         ekey.get());
+  SPG_CHECK_LAUNCH(ctx);
+  head.reset();
+  eidx.reset();
+  k2s.reset();
+  vs.reset();
+  DevBuf<uint8_t> flag(n_ent, ctx);
+  super_sb_heads<<<grid_for(n_ent, 256), 256, 0, ctx->stream>>>(ekey.get(), n_ent, flag.get());
+  SPG_CHECK_LAUNCH(ctx);
+  DevBuf<int64_t> heads(n_ent, ctx), n_sel(1, ctx);
+  thrust::counting_iterator<int64_t> it(0);
+  bytes = 0;
+  SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flag.get(), heads.get(), n_sel.get(),
+                                      n_ent, ctx->stream));
+  {
+    DevBuf<uint8_t> tmp(bytes, ctx);
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, flag.get(), heads.get(),
+                                        n_sel.get(), n_ent, ctx->stream));
+  }
+  ctx->lib_calls += 4;  // CUB device-wide primitives (library kernels)
+  const int64_t n_sb = copy_scalar_to_host_i64(ctx, n_sel.get());
+  DevBuf<int64_t> sb_offset(n_sb + 1, ctx);
+  DevBuf<uint64_t> sb_keys(n_sb, ctx);
+  super_sb_finish<<<grid_for(n_sb + 1, 256), 256, 0, ctx->stream>>>(
+      ekey.get(), heads.get(), n_sb, n_ent, sb_offset.get(), sb_keys.get());
+  SPG_CHECK_LAUNCH(ctx);
+  DevBuf<int32_t> sb_out(4 * n_sb, ctx);
+  SPG_CUDA(cudaMemsetAsync(sb_out.get(), 0xff, 4 * n_sb * sizeof(int32_t), ctx->stream));
+  super_out<<<grid_for(pl.n_out, 256), 256, 0, ctx->stream>>>(pl.out_keys.get(), pl.n_out,
+                                                              sb_keys.get(), n_sb, sb_out.get());
+  SPG_CHECK_LAUNCH(ctx);
+  DevBuf<int32_t> order = make_block_order(ctx, sb_keys.get(), n_sb, n_sb);
+  constexpr size_t smem = 2 * 4 * 32 * 36 * sizeof(double);
+  SPG_CUDA(cudaFuncSetAttribute(leaf_gemm_super32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_sb, int64_t(1) << 30));
+  leaf_gemm_super32<<<grid, 128, smem, ctx->stream>>>(A, btab, ent.get(), emask.get(),
+                                                       sb_offset.get(), sb_out.get(), n_sb, C,
+                                                       order.get());
+  SPG_CHECK_LAUNCH(ctx);
 }
 
 // The product streamed to host buffers: the GEMM runs in chunks of output
@@ -563,7 +727,8 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   const int L = a->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  Plan plan = plan_product(ctx, a, b, tau, skip_test, shard, false);
+  const bool super32 = L == 32 && !host && super32_enabled();
+  Plan plan = plan_product(ctx, a, b, tau, skip_test, shard, super32);
   const int64_t n_surv = plan.n_surv, n_out = plan.n_out;
   DevBuf<uint64_t>& out_keys = plan.out_keys;
   DevBuf<int64_t>& out_offset = plan.out_offset;
@@ -578,8 +743,11 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   } else {
     double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
     const double* const* btab = leaf_table(ctx, b);
-    DevBuf<int32_t> order = make_block_order(ctx, out_keys.get(), n_out, n_out);
-    {
+    if (super32) {
+      PhaseTrace tr(ctx, "gemm(super32)");
+      run_super32(ctx, a->depth, plan, a->payload, btab, c_payload);
+    } else {
+      DevBuf<int32_t> order = make_block_order(ctx, out_keys.get(), n_out, n_out);
       PhaseTrace tr(ctx, "gemm");
       run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload,
                nullptr, nullptr, 0, btab, order.get());

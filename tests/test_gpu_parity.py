@@ -213,6 +213,27 @@ def test_sweep_paths_in_subprocesses(port, env):
         assert got[name] == want, (env, name)
 
 
+@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_GEMM32": "3"}])
+def test_gemm_paths_in_subprocesses(env):
+    """Leaf-GEMM variants that keep every block's products in ascending k and
+    the same DMMA k-steps give C~ bit for bit equal to each other: the L = 32
+    super-block kernel (default) against per-block tilings; the variant is
+    fixed per process."""
+    import os
+    import subprocess
+    import sys as _sys
+    from pathlib import Path
+    script = Path(__file__).resolve().parent / "gemm_paths_case.py"
+
+    def run(extra):
+        out = subprocess.run([_sys.executable, str(script)], env={**os.environ, **extra},
+                             capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return out.stdout.split("\n")
+
+    assert run(env) == run({})
+
+
 def test_run_to_run_determinism(ctx):
     """SPEC determinism (test_multiply.cpp:140-156 analogue): repeated calls are
     bitwise identical."""
