@@ -431,8 +431,9 @@ struct SuperEntry {
 __global__ void __launch_bounds__(128, 3)
     leaf_gemm_super32(const double* __restrict__ A, const double* const* __restrict__ btab,
                       const SuperEntry* __restrict__ ent, const uint32_t* __restrict__ emask,
-                      const int64_t* __restrict__ sb_offset, const int32_t* __restrict__ sb_out,
-                      int64_t n_sb, double* __restrict__ C, const int32_t* __restrict__ order) {
+                      const int64_t* __restrict__ sb_beg, const int64_t* __restrict__ sb_end,
+                      const int32_t* __restrict__ sb_out, int64_t n_sb, double* __restrict__ C,
+                      const int32_t* __restrict__ order, int accumulate) {
   constexpr int L = 32, S = 36;  // leaf, padded stride (== 4 mod 16)
   constexpr int TILE = L * S;
   constexpr int STAGE = 4 * TILE;  // A row 0, A row 1, B col 0, B col 1
@@ -444,8 +445,12 @@ __global__ void __launch_bounds__(128, 3)
 
   for (int64_t sbi = blockIdx.x; sbi < n_sb; sbi += gridDim.x) {
     const int64_t sb = order ? order[sbi] : sbi;
-    const int64_t beg = sb_offset[sb];
-    const int64_t n = sb_offset[sb + 1] - beg;
+    // entries [sb_beg[sb], sb_end[sb]): all of the super block's, or those
+    // of one B panel (sb_end = sb_beg + 1 pointer for the whole list)
+    const int64_t beg = sb_beg[sb];
+    const int64_t n = sb_end[sb] - beg;
+    if (n == 0) continue;  // uniform per CTA
+    const int32_t o = sb_out[4 * sb + warp];
 
     auto load_stage = [&](const SuperEntry& en, uint32_t m, int stage) {
       double* st = smem + stage * STAGE;
@@ -472,7 +477,13 @@ __global__ void __launch_bounds__(128, 3)
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          acc[i][j][e] = (accumulate && o >= 0)
+                             ? C[static_cast<int64_t>(o) * LL +
+                                 static_cast<int64_t>(8 * j + perm8(2 * t + e)) * L + 8 * i + pg]
+                             : 0.0;
 
     // entries are fetched one step ahead, so their global latency hides
     // behind a compute step (as pr_next in leaf_gemm_dmma)
@@ -518,7 +529,6 @@ __global__ void __launch_bounds__(128, 3)
     }
     cp_async_wait<0>();
     __syncthreads();
-    const int32_t o = sb_out[4 * sb + warp];
     if (o >= 0) {
       double* Cblk = C + static_cast<int64_t>(o) * LL;
 #pragma unroll

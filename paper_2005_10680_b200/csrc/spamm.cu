@@ -366,7 +366,8 @@ __global__ void super_heads(const uint64_t* __restrict__ key2, int64_t n,
 __global__ void super_fill(const uint64_t* __restrict__ key2, const int64_t* __restrict__ val,
                            const int64_t* __restrict__ eidx, int64_t n, int kbits,
                            const int2* __restrict__ pairs, SuperEntry* __restrict__ ent,
-                           uint32_t* __restrict__ emask, uint64_t* __restrict__ ekey) {
+                           uint32_t* __restrict__ emask, uint64_t* __restrict__ ekey,
+                           uint32_t* __restrict__ ek) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const int64_t e = eidx[t] - 1;
@@ -379,7 +380,30 @@ __global__ void super_fill(const uint64_t* __restrict__ key2, const int64_t* __r
   if (sub & 1u) ent[e].b1 = pr.y;
   else ent[e].b0 = pr.y;
   atomicOr(&emask[e], 1u << sub);
-  if (t == 0 || (key2[t] >> 2) != (key2[t - 1] >> 2)) ekey[e] = key2[t] >> (kbits + 2);
+  if (t == 0 || (key2[t] >> 2) != (key2[t - 1] >> 2)) {
+    ekey[e] = key2[t] >> (kbits + 2);
+    ek[e] = static_cast<uint32_t>((key2[t] >> 2) & ((uint64_t(1) << kbits) - 1));
+  }
+}
+
+// per super block, the entry range whose k lies in [k0, k1) (a B panel)
+__global__ void super_panel_ranges(const uint32_t* __restrict__ ek,
+                                   const int64_t* __restrict__ sb_offset, int64_t n_sb,
+                                   uint32_t k0, uint32_t k1, int64_t* __restrict__ beg,
+                                   int64_t* __restrict__ end) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b >= n_sb) return;
+  auto lower = [&](uint32_t k) {
+    int64_t lo = sb_offset[b], hi = sb_offset[b + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (ek[mid] < k) lo = mid + 1;
+      else hi = mid;
+    }
+    return lo;
+  };
+  beg[b] = lower(k0);
+  end[b] = lower(k1);
 }
 
 __global__ void super_sb_heads(const uint64_t* __restrict__ ekey, int64_t n_ent,
@@ -528,10 +552,18 @@ bool super32_enabled() {
   return on;
 }
 
-void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,
-                 const double* const* btab, double* C) {
+struct Super32 {
+  int64_t n_sb = 0, n_ent = 0;
+  DevBuf<SuperEntry> ent;
+  DevBuf<uint32_t> emask, ek;
+  DevBuf<int64_t> sb_offset;
+  DevBuf<int32_t> sb_out, order;
+};
+
+Super32 build_super32(spg_context* ctx, int depth, const Plan& pl) {
+  Super32 sp;
   const int64_t n = pl.n_surv;
-  if (n == 0) return;
+  if (n == 0) return sp;
   const int kbits = pl.kbits;
   DevBuf<uint64_t> k2(n, ctx), k2s(n, ctx);
   DevBuf<int64_t> v(n, ctx), vs(n, ctx);
@@ -560,14 +592,16 @@ void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,
                                            ctx->stream));
   }
   const int64_t n_ent = copy_scalar_to_host_i64(ctx, eidx.get() + n - 1);
-  DevBuf<SuperEntry> ent(n_ent, ctx);
-  DevBuf<uint32_t> emask(n_ent, ctx);
+  sp.n_ent = n_ent;
+  sp.ent = DevBuf<SuperEntry>(n_ent, ctx);
+  sp.emask = DevBuf<uint32_t>(n_ent, ctx);
+  sp.ek = DevBuf<uint32_t>(n_ent, ctx);
   DevBuf<uint64_t> ekey(n_ent, ctx);
-  SPG_CUDA(cudaMemsetAsync(ent.get(), 0, n_ent * sizeof(SuperEntry), ctx->stream));
-  SPG_CUDA(cudaMemsetAsync(emask.get(), 0, n_ent * sizeof(uint32_t), ctx->stream));
+  SPG_CUDA(cudaMemsetAsync(sp.ent.get(), 0, n_ent * sizeof(SuperEntry), ctx->stream));
+  SPG_CUDA(cudaMemsetAsync(sp.emask.get(), 0, n_ent * sizeof(uint32_t), ctx->stream));
   super_fill<<<grid_for(n, 256), 256, 0, ctx->stream>>>(k2s.get(), vs.get(), eidx.get(), n, kbits,
-                                                         pl.pairs.get(), ent.get(), emask.get(),
-                                                         ekey.get());
+                                                         pl.pairs.get(), sp.ent.get(),
+                                                         sp.emask.get(), ekey.get(), sp.ek.get());
   SPG_CHECK_LAUNCH(ctx);
   head.reset();
   eidx.reset();
@@ -588,25 +622,43 @@ void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,
   }
   ctx->lib_calls += 4;  // CUB device-wide primitives (library kernels)
   const int64_t n_sb = copy_scalar_to_host_i64(ctx, n_sel.get());
-  DevBuf<int64_t> sb_offset(n_sb + 1, ctx);
+  sp.n_sb = n_sb;
+  sp.sb_offset = DevBuf<int64_t>(n_sb + 1, ctx);
   DevBuf<uint64_t> sb_keys(n_sb, ctx);
   super_sb_finish<<<grid_for(n_sb + 1, 256), 256, 0, ctx->stream>>>(
-      ekey.get(), heads.get(), n_sb, n_ent, sb_offset.get(), sb_keys.get());
+      ekey.get(), heads.get(), n_sb, n_ent, sp.sb_offset.get(), sb_keys.get());
   SPG_CHECK_LAUNCH(ctx);
-  DevBuf<int32_t> sb_out(4 * n_sb, ctx);
-  SPG_CUDA(cudaMemsetAsync(sb_out.get(), 0xff, 4 * n_sb * sizeof(int32_t), ctx->stream));
+  sp.sb_out = DevBuf<int32_t>(4 * n_sb, ctx);
+  SPG_CUDA(cudaMemsetAsync(sp.sb_out.get(), 0xff, 4 * n_sb * sizeof(int32_t), ctx->stream));
   super_out<<<grid_for(pl.n_out, 256), 256, 0, ctx->stream>>>(pl.out_keys.get(), pl.n_out,
-                                                              sb_keys.get(), n_sb, sb_out.get());
+                                                              sb_keys.get(), n_sb,
+                                                              sp.sb_out.get());
   SPG_CHECK_LAUNCH(ctx);
-  DevBuf<int32_t> order = make_block_order(ctx, sb_keys.get(), n_sb, n_sb);
+  sp.order = make_block_order(ctx, sb_keys.get(), n_sb, n_sb);
+  return sp;
+}
+
+// beg/end: per super block entry range (nullptr: all of its entries);
+// accumulate: continue the sub blocks' accumulators stored in C
+void launch_super32(spg_context* ctx, const Super32& sp, const double* A,
+                    const double* const* btab, double* C, const int64_t* beg = nullptr,
+                    const int64_t* end = nullptr, int accumulate = 0) {
+  if (sp.n_sb == 0) return;
   constexpr size_t smem = 2 * 4 * 32 * 36 * sizeof(double);
   SPG_CUDA(cudaFuncSetAttribute(leaf_gemm_super32, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(n_sb, int64_t(1) << 30));
-  leaf_gemm_super32<<<grid, 128, smem, ctx->stream>>>(A, btab, ent.get(), emask.get(),
-                                                       sb_offset.get(), sb_out.get(), n_sb, C,
-                                                       order.get());
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sp.n_sb, int64_t(1) << 30));
+  leaf_gemm_super32<<<grid, 128, smem, ctx->stream>>>(
+      A, btab, sp.ent.get(), sp.emask.get(), beg ? beg : sp.sb_offset.get(),
+      end ? end : sp.sb_offset.get() + 1, sp.sb_out.get(), sp.n_sb, C, sp.order.get(),
+      accumulate);
   SPG_CHECK_LAUNCH(ctx);
+}
+
+void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,
+                 const double* const* btab, double* C) {
+  const Super32 sp = build_super32(ctx, depth, pl);
+  launch_super32(ctx, sp, A, btab, C);
 }
 
 // The product streamed to host buffers: the GEMM runs in chunks of output
@@ -826,6 +878,9 @@ struct spg_plan {
   spg::DevBuf<int64_t> beg, end;
   spg::DevBuf<const double*> btab;  // B leaf addresses of the panels seen so far
   spg::DevBuf<int32_t> order;        // CTA order of the output blocks (row-major)
+  // L = 32: the 2x2 super-block entry list and its per-panel ranges
+  std::unique_ptr<spg::Super32> sup;
+  spg::DevBuf<int64_t> sb_beg, sb_end;
   int32_t next_row = 0;
   bool finished = false;
   spg_spamm_stats stats{};
@@ -883,7 +938,13 @@ spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b
   plan->beg = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
   plan->end = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
   plan->btab = DevBuf<const double*>(std::max<int64_t>(b->n_slots, 1), ctx);
-  plan->order = make_block_order(ctx, plan->pl.out_keys.get(), n_out, n_out);
+  if (a->leaf == 32 && super32_enabled() && plan->pl.n_surv) {
+    plan->sup = std::make_unique<Super32>(build_super32(ctx, a->depth, plan->pl));
+    plan->sb_beg = DevBuf<int64_t>(std::max<int64_t>(plan->sup->n_sb, 1), ctx);
+    plan->sb_end = DevBuf<int64_t>(std::max<int64_t>(plan->sup->n_sb, 1), ctx);
+  } else {
+    plan->order = make_block_order(ctx, plan->pl.out_keys.get(), n_out, n_out);
+  }
   SPG_CUDA(cudaEventSynchronize(ctx->ev[3]));
   spg_spamm_stats& st = plan->stats;
   st.survivors = plan->pl.n_surv;
@@ -922,16 +983,27 @@ void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_pan
   SPG_CUDA(cudaEventCreate(&pe.second));
   plan->panel_ev.push_back(pe);
   SPG_CUDA(cudaEventRecord(pe.first, ctx->stream));
-  panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
-      plan->pl.keys.get(), plan->pl.out_offset.get(), n_out, plan->pl.kbits,
-      static_cast<uint32_t>(r0), static_cast<uint32_t>(r1), plan->beg.get(), plan->end.get());
-  SPG_CHECK_LAUNCH(ctx);
   // pairs hold B slots; the panel buffer starts at slot lo
   leaf_ptr_kernel<<<grid_for(cnt, 256), 256, 0, ctx->stream>>>(d_panel, cnt, LL,
                                                               plan->btab.get() + lo);
   SPG_CHECK_LAUNCH(ctx);
-  run_gemm(ctx, L, plan->a->payload, nullptr, plan->pl.pairs.get(), plan->beg.get(), n_out,
-           plan->c.get(), ctx->stream, plan->end.get(), 1, plan->btab.get(), plan->order.get());
+  if (plan->sup) {
+    const Super32& sp = *plan->sup;
+    super_panel_ranges<<<grid_for(std::max<int64_t>(sp.n_sb, 1), 256), 256, 0, ctx->stream>>>(
+        sp.ek.get(), sp.sb_offset.get(), sp.n_sb, static_cast<uint32_t>(r0),
+        static_cast<uint32_t>(r1), plan->sb_beg.get(), plan->sb_end.get());
+    SPG_CHECK_LAUNCH(ctx);
+    launch_super32(ctx, sp, plan->a->payload, plan->btab.get(), plan->c.get(),
+                   plan->sb_beg.get(), plan->sb_end.get(), 1);
+  } else {
+    panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
+        plan->pl.keys.get(), plan->pl.out_offset.get(), n_out, plan->pl.kbits,
+        static_cast<uint32_t>(r0), static_cast<uint32_t>(r1), plan->beg.get(), plan->end.get());
+    SPG_CHECK_LAUNCH(ctx);
+    run_gemm(ctx, L, plan->a->payload, nullptr, plan->pl.pairs.get(), plan->beg.get(), n_out,
+             plan->c.get(), ctx->stream, plan->end.get(), 1, plan->btab.get(),
+             plan->order.get());
+  }
   SPG_CUDA(cudaEventRecord(pe.second, ctx->stream));
 }
 
@@ -951,9 +1023,12 @@ void plan_run_table(spg_plan* plan, const double* const* h_table, int64_t n_tabl
                            cudaMemcpyHostToDevice, ctx->stream));
   SPG_CUDA(cudaEventRecord(plan->t_first, ctx->stream));
   plan->started = true;
-  run_gemm(ctx, plan->a->leaf, plan->a->payload, nullptr, plan->pl.pairs.get(),
-           plan->pl.out_offset.get(), n_out, plan->c.get(), ctx->stream, nullptr, 0, d_tab.get(),
-           plan->order.get());
+  if (plan->sup)
+    launch_super32(ctx, *plan->sup, plan->a->payload, d_tab.get(), plan->c.get());
+  else
+    run_gemm(ctx, plan->a->leaf, plan->a->payload, nullptr, plan->pl.pairs.get(),
+             plan->pl.out_offset.get(), n_out, plan->c.get(), ctx->stream, nullptr, 0,
+             d_tab.get(), plan->order.get());
   SPG_CUDA(cudaStreamSynchronize(ctx->stream));  // the table buffer returns to the pool
 }
 
