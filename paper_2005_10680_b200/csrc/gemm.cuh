@@ -68,7 +68,13 @@ struct DmmaGemmCfg {
 // allocations, e.g. peer GPUs' memory mapped over NVLink, or a matrix's own
 // leaf table: the table form also measured 3.6 % faster on cfg2 -- the loaded
 // pointer spares the per-copy 64-bit address rematerialisation of B + y L^2).
-template <int L, int KC, int WM, int WN, int NSTAGE, bool kTable = false>
+// LD > L: the operands and outputs are L x L sub-blocks of LD x LD leaves
+// (column-major, leading dimension LD).  Pair (ax, by) then names A sub-block
+// (ax/4, k-half (ax/2)&1, row half ax&1) and B sub-block (by/4, k-half
+// (by/2)&1, column half by&1), and output o is sub-block (o/4, row half
+// (o/2)&1, column half o&1) -- so L = 128 leaves run as L = 64 products with
+// the same per-element DMMA sequence (leaf_gemm_dmma<64, ..., 128>).
+template <int L, int KC, int WM, int WN, int NSTAGE, bool kTable = false, int LD = L>
 __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
                                   (L > 64) ? 1 : ((L / WM) * (L / WN) <= 4 ? 3 : 2))
     leaf_gemm_dmma(const double* __restrict__ A, const double* __restrict__ B,
@@ -84,7 +90,12 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
   const int pg = perm8(g);
   const int m0 = (warp % Cfg::WARPS_M) * WM;
   const int n0 = (warp / Cfg::WARPS_M) * WN;
-  constexpr int64_t LL = static_cast<int64_t>(L) * L;
+  constexpr int64_t LL = static_cast<int64_t>(LD) * LD;  // leaf stride
+  static_assert(LD == L || LD == 2 * L, "sub-blocks: halves of the leaf");
+  // offset of sub-block (row half r, column half c) inside a leaf
+  auto sub_off = [](int64_t idx, int r, int c) -> int64_t {
+    return LD == L ? 0 : static_cast<int64_t>(c) * L * LD + static_cast<int64_t>(r) * L;
+  };
 
   for (int64_t ob = blockIdx.x; ob < n_out; ob += gridDim.x) {
     const int64_t o = order ? order[ob] : ob;
@@ -101,7 +112,9 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
     };
     auto load_stage = [&](Src pr, int64_t step, int stage) {
       const int c = static_cast<int>(step % Cfg::CHUNKS);
-      const double* Ablk = A + static_cast<int64_t>(pr.ax) * LL + static_cast<int64_t>(c) * KC * L;
+      const double* Ablk = A + static_cast<int64_t>(LD == L ? pr.ax : (pr.ax >> 2)) * LL +
+                           (LD == L ? 0 : sub_off(0, pr.ax & 1, (pr.ax >> 1) & 1)) +
+                           static_cast<int64_t>(c) * KC * LD;
       const double* Bblk = pr.b + c * KC;
       double* As = smem + stage * Cfg::STAGE;
       double* Bs = As + Cfg::A_STAGE;
@@ -109,17 +122,22 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
 #pragma unroll
       for (int p = tid; p < A_PIECES; p += Cfg::kThreads) {
         const int kk = p / (L / 2), off = (p % (L / 2)) * 2;
-        cp_async16(As + kk * Cfg::AS + off, Ablk + kk * L + off);
+        cp_async16(As + kk * Cfg::AS + off, Ablk + kk * LD + off);
       }
       constexpr int B_PIECES = L * KC / 2;
 #pragma unroll
       for (int p = tid; p < B_PIECES; p += Cfg::kThreads) {
         const int j = p / (KC / 2), off = (p % (KC / 2)) * 2;
-        cp_async16(Bs + j * Cfg::BS + off, Bblk + static_cast<int64_t>(j) * L + off);
+        cp_async16(Bs + j * Cfg::BS + off, Bblk + static_cast<int64_t>(j) * LD + off);
       }
     };
     auto pair_of = [&](int64_t step) -> Src {
       const int2 pr = step < nsteps ? __ldg(pairs + beg + step / Cfg::CHUNKS) : make_int2(0, 0);
+      if constexpr (LD != L) {
+        // B sub-block: leaf pr.y/4, k-half (pr.y/2)&1 (rows), column half pr.y&1
+        const double* leaf = step < nsteps ? btab[pr.y >> 2] : B;
+        return Src{pr.x, leaf + sub_off(0, (pr.y >> 1) & 1, pr.y & 1)};
+      }
       if constexpr (kTable) return Src{pr.x, step < nsteps ? btab[pr.y] : B};
       return Src{pr.x, B + static_cast<int64_t>(pr.y) * LL};
     };
@@ -131,7 +149,8 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
       for (int j = 0; j < Cfg::TN; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          acc[i][j][e] = accumulate ? C[o * LL + static_cast<int64_t>(n0 + 8 * j + perm8(2 * t + e)) * L +
+          acc[i][j][e] = accumulate ? C[(LD == L ? o * LL : (o >> 2) * LL + sub_off(0, (o >> 1) & 1, o & 1)) +
+                                        static_cast<int64_t>(n0 + 8 * j + perm8(2 * t + e)) * LD +
                                         m0 + 8 * i + pg]
                                     : 0.0;
 
@@ -168,7 +187,7 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
     cp_async_wait<0>();
     __syncthreads();
 
-    double* Cblk = C + o * LL;
+    double* Cblk = C + (LD == L ? o * LL : (o >> 2) * LL + sub_off(0, (o >> 1) & 1, o & 1));
 #pragma unroll
     for (int i = 0; i < Cfg::TM; ++i)
 #pragma unroll
@@ -177,7 +196,7 @@ __global__ void __launch_bounds__(32 * (L / WM) * (L / WN),
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int col = n0 + 8 * j + perm8(2 * t + e);
-          Cblk[static_cast<int64_t>(col) * L + row] = acc[i][j][e];
+          Cblk[static_cast<int64_t>(col) * LD + row] = acc[i][j][e];
         }
       }
   }

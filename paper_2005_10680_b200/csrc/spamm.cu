@@ -438,6 +438,33 @@ __global__ void super_out(const uint64_t* __restrict__ out_keys, int64_t n_out,
   sb_out[4 * lo + static_cast<int64_t>(out_keys[o] & 3u)] = static_cast<int32_t>(o);
 }
 
+// ---- L = 128 leaves as 2x2 x 2 L = 64 sub-products (leaf_gemm_dmma<64, ..., 128>):
+// output o -> sub outputs 4o + (2a + b); product (x, y) -> for k-half h the
+// sub pair (4x + 2h + a, 4y + 2h + b); per sub output the original pairs in
+// order, h = 0 then 1 (the L = 128 kernel's k order).
+__global__ void expand_sub128(const int2* __restrict__ pairs,
+                              const int64_t* __restrict__ out_offset,
+                              const uint64_t* __restrict__ out_keys, int64_t n_out,
+                              int2* __restrict__ sub_pairs, int64_t* __restrict__ sub_offset,
+                              uint64_t* __restrict__ sub_keys) {
+  for (int64_t o = blockIdx.x; o < n_out; o += gridDim.x) {
+    const int64_t beg = out_offset[o], cnt = out_offset[o + 1] - beg;
+    if (threadIdx.x < 4) {
+      sub_offset[4 * o + threadIdx.x] = 8 * beg + threadIdx.x * 2 * cnt;
+      sub_keys[4 * o + threadIdx.x] = (out_keys[o] << 2) | threadIdx.x;
+    }
+    if (o == n_out - 1 && threadIdx.x == 0) sub_offset[4 * n_out] = 8 * (beg + cnt);
+    for (int64_t q = threadIdx.x; q < 8 * cnt; q += blockDim.x) {
+      const int64_t p = q >> 3;
+      const int s = static_cast<int>((q >> 1) & 3), h = static_cast<int>(q & 1);
+      const int a = s >> 1, b = s & 1;
+      const int2 pr = pairs[beg + p];
+      sub_pairs[8 * beg + s * 2 * cnt + 2 * p + h] =
+          make_int2(4 * pr.x + 2 * h + a, 4 * pr.y + 2 * h + b);
+    }
+  }
+}
+
 struct Plan {
   int64_t n_surv = 0, n_out = 0;
   int kbits = 0;
@@ -661,6 +688,78 @@ void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,
   launch_super32(ctx, sp, A, btab, C);
 }
 
+// L = 128 products as L = 64 sub-products (the default; another SPG_GEMM128
+// value selects an L = 128 tiling): one L = 64 CTA per output sub-block,
+// three per SM, where the L = 128 kernel fits one (registers) and idles the
+// DMMA pipe between blocks.  Config-5 style L = 128 product
+// (tools/profile_leaf.py 128): 32.7 -> 34.8 TFLOP/s, C~ bitwise unchanged.
+bool sub128_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPG_GEMM128");
+    return !e || std::atoi(e) == 9;
+  }();
+  return on;
+}
+
+struct Sub128 {
+  int64_t n_sub = 0;
+  DevBuf<int2> pairs;
+  DevBuf<int64_t> offset;  // 4 n_out + 1
+  DevBuf<int32_t> order;
+};
+
+Sub128 build_sub128(spg_context* ctx, const Plan& pl) {
+  Sub128 sb;
+  const int64_t n_out = pl.n_out;
+  if (n_out == 0) return sb;
+  sb.n_sub = 4 * n_out;
+  sb.pairs = DevBuf<int2>(std::max<int64_t>(8 * pl.n_surv, 1), ctx);
+  sb.offset = DevBuf<int64_t>(4 * n_out + 1, ctx);
+  DevBuf<uint64_t> sk(4 * n_out, ctx);
+  expand_sub128<<<static_cast<unsigned>(std::min<int64_t>(n_out, 1 << 20)), 256, 0,
+                  ctx->stream>>>(pl.pairs.get(), pl.out_offset.get(), pl.out_keys.get(), n_out,
+                                 sb.pairs.get(), sb.offset.get(), sk.get());
+  SPG_CHECK_LAUNCH(ctx);
+  sb.order = make_block_order(ctx, sk.get(), 4 * n_out, 4 * n_out);
+  return sb;
+}
+
+// beg/end: per sub output pair range (beg = offset, end = nullptr: all)
+void launch_sub128(spg_context* ctx, const Sub128& sb, const double* A, const double* const* btab,
+                   double* C, const int64_t* beg = nullptr, const int64_t* end = nullptr,
+                   int accumulate = 0) {
+  if (sb.n_sub == 0) return;
+  using Cfg = DmmaGemmCfg<64, 32, 32, 32, 2>;
+  auto kern = leaf_gemm_dmma<64, 32, 32, 32, 2, true, 128>;
+  SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Cfg::kSmemBytes)));
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sb.n_sub, int64_t(1) << 30));
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, ctx->stream>>>(
+      A, nullptr, sb.pairs.get(), beg ? beg : sb.offset.get(), sb.n_sub, C, end, accumulate,
+      btab, sb.order.get());
+  SPG_CHECK_LAUNCH(ctx);
+}
+
+// a B panel's per-block pair ranges [bbeg, bend) -> the sub outputs' ranges
+__global__ void sub128_ranges(const int64_t* __restrict__ out_offset,
+                              const int64_t* __restrict__ bbeg, const int64_t* __restrict__ bend,
+                              int64_t n_out, int64_t* __restrict__ sbeg,
+                              int64_t* __restrict__ send) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= 4 * n_out) return;
+  const int64_t o = q >> 2, s = q & 3;
+  const int64_t b0 = out_offset[o], cnt = out_offset[o + 1] - b0;
+  const int64_t base = 8 * b0 + s * 2 * cnt;
+  sbeg[q] = base + 2 * (bbeg[o] - b0);
+  send[q] = base + 2 * (bend[o] - b0);
+}
+
+void run_sub128(spg_context* ctx, const Plan& pl, const double* A, const double* const* btab,
+                double* C) {
+  const Sub128 sb = build_sub128(ctx, pl);
+  launch_sub128(ctx, sb, A, btab, C);
+}
+
 // The product streamed to host buffers: the GEMM runs in chunks of output
 // blocks (Morton order); after each chunk its leaf norms are computed (K1)
 // and the chunk is copied D2H on the copy stream while the next chunk
@@ -798,6 +897,9 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     if (super32) {
       PhaseTrace tr(ctx, "gemm(super32)");
       run_super32(ctx, a->depth, plan, a->payload, btab, c_payload);
+    } else if (L == 128 && sub128_enabled()) {
+      PhaseTrace tr(ctx, "gemm(sub128)");
+      run_sub128(ctx, plan, a->payload, btab, c_payload);
     } else {
       DevBuf<int32_t> order = make_block_order(ctx, out_keys.get(), n_out, n_out);
       PhaseTrace tr(ctx, "gemm");
@@ -881,6 +983,9 @@ struct spg_plan {
   // L = 32: the 2x2 super-block entry list and its per-panel ranges
   std::unique_ptr<spg::Super32> sup;
   spg::DevBuf<int64_t> sb_beg, sb_end;
+  // L = 128: the L = 64 sub-product list and its per-panel ranges
+  std::unique_ptr<spg::Sub128> sub;
+  spg::DevBuf<int64_t> sub_beg, sub_end;
   int32_t next_row = 0;
   bool finished = false;
   spg_spamm_stats stats{};
@@ -938,7 +1043,11 @@ spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b
   plan->beg = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
   plan->end = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
   plan->btab = DevBuf<const double*>(std::max<int64_t>(b->n_slots, 1), ctx);
-  if (a->leaf == 32 && super32_enabled() && plan->pl.n_surv) {
+  if (a->leaf == 128 && sub128_enabled() && plan->pl.n_surv) {
+    plan->sub = std::make_unique<Sub128>(build_sub128(ctx, plan->pl));
+    plan->sub_beg = DevBuf<int64_t>(std::max<int64_t>(plan->sub->n_sub, 1), ctx);
+    plan->sub_end = DevBuf<int64_t>(std::max<int64_t>(plan->sub->n_sub, 1), ctx);
+  } else if (a->leaf == 32 && super32_enabled() && plan->pl.n_surv) {
     plan->sup = std::make_unique<Super32>(build_super32(ctx, a->depth, plan->pl));
     plan->sb_beg = DevBuf<int64_t>(std::max<int64_t>(plan->sup->n_sb, 1), ctx);
     plan->sb_end = DevBuf<int64_t>(std::max<int64_t>(plan->sup->n_sb, 1), ctx);
@@ -995,6 +1104,17 @@ void plan_accumulate(spg_plan* plan, int32_t r0, int32_t r1, const double* d_pan
     SPG_CHECK_LAUNCH(ctx);
     launch_super32(ctx, sp, plan->a->payload, plan->btab.get(), plan->c.get(),
                    plan->sb_beg.get(), plan->sb_end.get(), 1);
+  } else if (plan->sub) {
+    panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
+        plan->pl.keys.get(), plan->pl.out_offset.get(), n_out, plan->pl.kbits,
+        static_cast<uint32_t>(r0), static_cast<uint32_t>(r1), plan->beg.get(), plan->end.get());
+    SPG_CHECK_LAUNCH(ctx);
+    sub128_ranges<<<grid_for(4 * n_out, 256), 256, 0, ctx->stream>>>(
+        plan->pl.out_offset.get(), plan->beg.get(), plan->end.get(), n_out,
+        plan->sub_beg.get(), plan->sub_end.get());
+    SPG_CHECK_LAUNCH(ctx);
+    launch_sub128(ctx, *plan->sub, plan->a->payload, plan->btab.get(), plan->c.get(),
+                  plan->sub_beg.get(), plan->sub_end.get(), 1);
   } else {
     panel_ranges<<<grid_for(n_out, 256), 256, 0, ctx->stream>>>(
         plan->pl.keys.get(), plan->pl.out_offset.get(), n_out, plan->pl.kbits,
@@ -1025,6 +1145,8 @@ void plan_run_table(spg_plan* plan, const double* const* h_table, int64_t n_tabl
   plan->started = true;
   if (plan->sup)
     launch_super32(ctx, *plan->sup, plan->a->payload, d_tab.get(), plan->c.get());
+  else if (plan->sub)
+    launch_sub128(ctx, *plan->sub, plan->a->payload, d_tab.get(), plan->c.get());
   else
     run_gemm(ctx, plan->a->leaf, plan->a->payload, nullptr, plan->pl.pairs.get(),
              plan->pl.out_offset.get(), n_out, plan->c.get(), ctx->stream, nullptr, 0,
