@@ -6,8 +6,8 @@ import subprocess
 import sys
 
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-var = {32: ("SPG_GEMM32", [6, 2, 8, 1, 7]), 64: ("SPG_GEMM", [4, 5, 6, 8]),
-       128: ("SPG_GEMM128", [3, 4, 1, 2])}[L]
+var = {32: ("SPG_GEMM32", [9, 6, 2, 8, 1, 7]), 64: ("SPG_GEMM", [4, 5, 6, 8]),
+       128: ("SPG_GEMM128", [9, 3, 4, 1, 2])}[L]
 code = f"""
 import sys
 sys.path.insert(0, {os.path.dirname(os.path.dirname(os.path.abspath(__file__)))!r})
