@@ -48,6 +48,9 @@ ap.add_argument("--panel-rows", type=int, default=None)
 ap.add_argument("--row-chunks", type=int, default=8)
 ap.add_argument("--tau-lo", type=float, default=None)
 ap.add_argument("--deltas", default=None)
+ap.add_argument("--all-ranks", action="store_true",
+                help="run every rank's share in turn (tables built once): the projected "
+                     "8-GPU time is the slowest rank")
 args = ap.parse_args()
 cfg5 = args.config == 5
 N = args.n or (131072 if cfg5 else 262144)
@@ -76,11 +79,12 @@ sB = nat.synth_cluster_scale(ctx, N, ELL, DENS, SITE, SEED_B)
 nb = N // L
 rows_per = nb // ranks
 tabA, tabB, A_local = [], [], None
+run_ranks = list(range(ranks)) if args.all_ranks else [rank]
 for g in range(ranks):
     lo, hi = g * rows_per, (g + 1) * rows_per
     Ag = nat.synth_cluster_device_rows_scaled(ctx, N, L, ELL, DENS, SITE, SEED_A, DROP, sA, lo, hi)
     tabA.append(leaf_table(Ag))
-    if g == rank:
+    if g == run_ranks[0]:
         A_local = Ag
     else:
         Ag.free()
@@ -125,30 +129,48 @@ def fetch(r0, r1, owner, buf, count, stream):
 
 
 sched = panel_schedule(N, L, 0, panel_rows)
-for delta in deltas:
-    out = dict(base)
-    out["delta"] = delta
-    tau, k = nat.select_tolerance(bounds, taus, delta)
-    out["tau"], out["tau_index"] = tau, k
-    out["bound"] = float(bounds[k]) if k >= 0 else 0.0
-    tot = {"candidates": 0, "survivors": 0, "flops": 0.0, "ms_gemm": 0.0, "ms_tasklist": 0.0,
-           "ms_finalize": 0.0, "output_blocks": 0}
-    t3 = time.perf_counter()
-    for sub in range(row_chunks):
-        plan = nat.Plan(ctx, A_local, B_norms, tau, level + c, (rank << c) + sub, a_norms=A_norms)
-        run_panels(ctx, plan, sched, fetch, L)
-        C, st = plan.finish()
-        plan.free()
-        for key in tot:
-            tot[key] += st[key]
-        C.free()
-    ctx.synchronize()
-    out["product_wall_s"] = round(time.perf_counter() - t3, 2)
-    out.update({k2: (round(v, 1) if isinstance(v, float) else v) for k2, v in tot.items()})
-    out["skipped_fraction"] = round(1 - tot["survivors"] / max(tot["candidates"], 1), 4)
-    # ms_gemm: the panel GEMM launches' kernel time; the wall time also holds
-    # generating the B panels on the device (the owners' broadcasts on 8 GPUs)
-    out["gemm_tflops"] = round(tot["flops"] / tot["ms_gemm"] / 1e9, 2) if tot["ms_gemm"] else 0.0
-    out["wall_tflops_incl_panel_generation"] = round(tot["flops"] / out["product_wall_s"] / 1e12, 2)
-    out["sweep_shard_eff_gbs"] = round(12 * tot["candidates"] / (out["sweep_shard_ms"] / 1e3) / 1e9, 1)
-    print(json.dumps(out), flush=True)
+for rk in run_ranks:
+    if A_local is None:
+        A_local = nat.synth_cluster_device_rows_scaled(ctx, N, L, ELL, DENS, SITE, SEED_A, DROP, sA,
+                                                       rk * rows_per, (rk + 1) * rows_per)
+    if rk != rank:
+        ctx.synchronize()
+        t1 = time.perf_counter()
+        nat.cse_shard(ctx, A_norms, B_norms, taus, level, rk)
+        ctx.synchronize()
+        base["sweep_shard_ms"] = round(1e3 * (time.perf_counter() - t1), 3)
+    base["rank"] = rk
+    base["leaves_A_rank"] = int(A_local.nnz_blocks)
+    for delta in deltas:
+        out = dict(base)
+        out["delta"] = delta
+        tau, k = nat.select_tolerance(bounds, taus, delta)
+        out["tau"], out["tau_index"] = tau, k
+        out["bound"] = float(bounds[k]) if k >= 0 else 0.0
+        tot = {"candidates": 0, "survivors": 0, "flops": 0.0, "ms_gemm": 0.0, "ms_tasklist": 0.0,
+               "ms_finalize": 0.0, "output_blocks": 0}
+        t3 = time.perf_counter()
+        for sub in range(row_chunks):
+            plan = nat.Plan(ctx, A_local, B_norms, tau, level + c, (rk << c) + sub,
+                            a_norms=A_norms)
+            run_panels(ctx, plan, sched, fetch, L)
+            C, st = plan.finish()
+            plan.free()
+            for key in tot:
+                tot[key] += st[key]
+            C.free()
+        ctx.synchronize()
+        out["product_wall_s"] = round(time.perf_counter() - t3, 2)
+        out.update({k2: (round(v, 1) if isinstance(v, float) else v) for k2, v in tot.items()})
+        out["skipped_fraction"] = round(1 - tot["survivors"] / max(tot["candidates"], 1), 4)
+        # ms_gemm: the panel GEMM launches' kernel time; the wall time also holds
+        # generating the B panels on the device (the owners' broadcasts on 8 GPUs)
+        out["gemm_tflops"] = (round(tot["flops"] / tot["ms_gemm"] / 1e9, 2) if tot["ms_gemm"]
+                              else 0.0)
+        out["wall_tflops_incl_panel_generation"] = round(
+            tot["flops"] / out["product_wall_s"] / 1e12, 2)
+        out["sweep_shard_eff_gbs"] = round(
+            12 * tot["candidates"] / (out["sweep_shard_ms"] / 1e3) / 1e9, 1)
+        print(json.dumps(out), flush=True)
+    A_local.free()
+    A_local = None
