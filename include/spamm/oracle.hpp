@@ -1,11 +1,14 @@
 #pragma once
 //
-// spamm-b200 drop-in: the reference's dense helpers and synthetic-instance
-// generator (/root/reference/proj/core/include/spamm/oracle.hpp, src/oracle.cpp),
-// which its experiment runner uses for generated inputs, spectral bounds and
-// the small-N density-matrix check.  Host code on dense matrices -- never on
-// the GPU product path.  generate_decay_matrix reproduces the reference's bits
-// for a given seed (mt19937_64 stream, 53-bit mapping, same arithmetic order).
+// The reference's dense test helpers (/root/reference/proj/core/include/spamm/
+// oracle.hpp): declarations only.  They are the reference's test oracle, so the
+// product library (libspamm_ec.so) does NOT define them.  Link a build of the
+// unmodified reference src/oracle.cpp against these headers (oracle/Makefile
+// target `ref` builds oracle/_ref/libspamm_dense_oracle.so -- test
+// infrastructure) and hand the functions to the experiment runners with
+// spamm::set_experiment_oracle (experiment.hpp).  DecayModelSpec stays here
+// because ExperimentConfig carries it.  Gershgorin bounds of a quadtree matrix
+// are computed on the device by spamm::gershgorin_bounds (quadtree.hpp).
 //
 #include <cstdint>
 #include <utility>

@@ -11,13 +11,14 @@
 // (include/spamm_gpu.h: packed FP64 leaf payload + dense Morton norm pyramid
 // in HBM) built by the CUDA norm kernels.  The host Node tree that root()
 // exposes is materialised lazily, only when a caller walks it; products,
-// the CSE sweep and tolerance selection never leave the device.  Host trees
-// assembled with wrap() are uploaded on first use.
+// the CSE sweep, tolerance selection, trace, nnz, scale and add never leave
+// the device.  Host trees assembled with wrap() are uploaded on first use.
 //
 #include <array>
 #include <cstdint>
 #include <memory>
 #include <span>
+#include <utility>
 #include <vector>
 
 #include "spamm/dense_matrix.hpp"
@@ -87,8 +88,13 @@ class QuadTreeMatrix {
   friend QuadTreeMatrix adopt_device(spg_matrix* m);
 };
 
-/// Entrywise sum (host operation, not on the GPU hot path).
+/// Entrywise sum (add_nodes, quadtree.cpp:24-36), computed on the device.
 QuadTreeMatrix add(const QuadTreeMatrix& a, const QuadTreeMatrix& b);
+
+/// B200 extension: Gershgorin spectral bounds {low, high} computed from the
+/// device leaves -- bitwise the reference's oracle::gershgorin_bounds on
+/// a.to_dense() (oracle.cpp:191-200) without building the dense matrix.
+std::pair<double, double> gershgorin_bounds(const QuadTreeMatrix& a);
 
 /// B200 extension: wrap a device matrix returned by the C ABI.
 QuadTreeMatrix adopt_device(spg_matrix* m);

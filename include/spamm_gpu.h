@@ -219,6 +219,11 @@ int spg_matrix_from_diagonal(spg_context* ctx, int32_t dimension, int32_t leaf_s
 /* Per row i (host arrays of length n, either may be NULL): the diagonal entry
  * and sum_j |a_ij| (ascending j) -- Gershgorin data for spectral bounds. */
 int spg_matrix_rows(const spg_matrix* m, double* diag, double* abs_row_sums);
+/* Gershgorin spectral bounds (reference oracle.cpp:191-200 on the dense
+ * matrix): low = min_i (a_ii - r_i), high = max_i (a_ii + r_i), r_i = sum over
+ * j != i of |a_ij| in ascending j -- bitwise the reference's values, computed
+ * from the device leaves (no dense copy). */
+int spg_matrix_gershgorin(const spg_matrix* m, double* low, double* high);
 
 /* ---- SP2 purification over the GPU product (purification.cpp:49-202;
  * SURVEY.md 8f row 2, BASELINE config 3) ----------------------------------- */
@@ -361,7 +366,8 @@ int spg_matrix_payload_slots(const spg_matrix* m, int32_t* slots);
 int spg_ipc_export(const spg_matrix* m, void* handle);
 int spg_ipc_open(spg_context* ctx, const void* handle, const double** base);
 int spg_ipc_close(spg_context* ctx, const double* base);
-/* Norm-only matrix from a leaf table (host arrays, sorted by block row; slot
+/* Norm-only matrix from a leaf table (host arrays, sorted by (block row, block
+ * col), no duplicates -- SPG_EINVAL otherwise; slot
  * t = leaf t).  nonzero may be NULL (every leaf non-null).  Norms are taken
  * as given: pass the block_norm values the owning GPU computed (download
  * norms) for bit-exact bounds. */

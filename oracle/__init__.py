@@ -124,6 +124,9 @@ class Oracle:
         else:
             self._from_dense = fn("from_dense", _vp, [C.c_int, C.c_int, _dp])
             self._threads = fn("set_max_threads", None, [C.c_int])
+            self._trace = fn("trace", C.c_double, [_vp])
+            self._nnz_entries = fn("nnz", C.c_int64, [_vp])
+            self._axpby = fn("axpby", _vp, [C.c_double, _vp, C.c_double, _vp])
             self._purify = fn("purify", _vp, [_vp, C.c_int, C.c_int, C.c_int, C.c_double, _dp,
                                               C.c_int, C.c_double, _dp, C.c_double, C.c_int,
                                               C.POINTER(C.c_int), _dp, C.POINTER(C.c_int),
@@ -152,6 +155,19 @@ class Oracle:
         if not h:
             raise ValueError("oracle build rejected the leaf list")
         return Tree(self, h, leaf)
+
+    # -- algebra the callers use (ref back end only) ----------------------------
+    def trace(self, a: Tree) -> float:
+        return self._trace(a.h)
+
+    def nnz(self, a: Tree) -> int:
+        return self._nnz_entries(a.h)
+
+    def axpby(self, alpha: float, a: Tree, beta: float = 0.0, b: Tree | None = None) -> Tree:
+        h = self._axpby(alpha, a.h, beta, b.h if b is not None else None)
+        if not h:
+            raise ValueError("axpby: invalid arguments")
+        return Tree(self, h, a.leaf)
 
     def set_threads(self, n: int):
         if self.kind == "ref":

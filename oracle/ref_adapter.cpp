@@ -221,6 +221,25 @@ void ref_level_norms(const void* t, int level, double* out) {
   walk_level(r->m.root(), 0, level, 0, out);
 }
 
+// QuadTreeMatrix::trace / nnz (quadtree.cpp:231-233)
+double ref_trace(const void* t) { return static_cast<const RefTree*>(t)->m.trace(); }
+std::int64_t ref_nnz(const void* t) { return static_cast<const RefTree*>(t)->m.nnz(); }
+
+// add(a.scale(alpha), b.scale(beta)) (quadtree.cpp:249-261); b may be null
+void* ref_axpby(double alpha, const void* a, double beta, const void* b) {
+  try {
+    const auto* ra = static_cast<const RefTree*>(a);
+    auto* out = new RefTree;
+    out->depth = ra->depth;
+    QuadTreeMatrix x = ra->m.scale(alpha);
+    if (b) x = spamm::add(x, static_cast<const RefTree*>(b)->m.scale(beta));
+    out->m = std::move(x);
+    return out;
+  } catch (const std::exception&) {
+    return nullptr;
+  }
+}
+
 // spamm::cse (error_control.cpp:160-166)
 int ref_cse(const void* a, const void* b, const double* taus, int n, double* bounds) {
   try {

@@ -178,6 +178,7 @@ _SIGNATURES = {
     "spg_staged_free": (None, [_vp]),
     "spg_matrix_from_diagonal": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.POINTER(_vp)]),
     "spg_matrix_rows": (C.c_int, [_vp, _dp, _dp]),
+    "spg_matrix_gershgorin": (C.c_int, [_vp, _dp, _dp]),
     "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
                                              _dp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
     "spg_matrix_gather_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64, _vp]),
@@ -589,6 +590,13 @@ def row_data(m: Matrix):
     a = np.empty(n, np.float64)
     _check(lib().spg_matrix_rows(m.handle, _ptr(d, C.c_double), _ptr(a, C.c_double)))
     return d, a
+
+
+def gershgorin(m: Matrix):
+    """(low, high) Gershgorin spectral bounds, reference oracle.cpp:191-200."""
+    lo, hi = C.c_double(), C.c_double()
+    _check(lib().spg_matrix_gershgorin(m.handle, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 def identity(ctx: Context, n: int, leaf: int) -> Matrix:

@@ -35,7 +35,7 @@ HEADERS = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)
 
 CXX = os.environ.get("CXX", "g++")
 DROPIN_SOURCES = ["dropin/quadtree.cpp", "dropin/multiply.cpp", "dropin/error_control.cpp",
-                  "dropin/matrix_market.cpp", "dropin/oracle.cpp", "dropin/experiment.cpp",
+                  "dropin/matrix_market.cpp", "dropin/experiment.cpp",
                   "dropin/purification.cpp", "dropin/runtime.cpp"]
 
 
@@ -79,7 +79,7 @@ def build_dropin() -> Path:
     LIB.mkdir(parents=True, exist_ok=True)
     srcs = [CSRC / s for s in DROPIN_SOURCES]
     out = LIB / "libspamm_ec.so"
-    hdrs = list((INCLUDE / "spamm").glob("*.hpp")) + HEADERS
+    hdrs = list((INCLUDE / "spamm").glob("*.hpp")) + list((CSRC / "dropin").glob("*.hpp")) + HEADERS
     gpu = LIB / "libspamm_gpu.so"
     if _stale(out, srcs + hdrs + [gpu]):
         _run([CXX, "-std=c++20", "-O2", "-fPIC", "-shared", "-ffp-contract=off",

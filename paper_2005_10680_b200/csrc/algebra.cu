@@ -12,6 +12,7 @@
 #include <thrust/iterator/counting_iterator.h>
 
 #include <algorithm>
+#include <limits>
 #include <vector>
 
 #include "common.cuh"
@@ -77,10 +78,12 @@ __global__ void axpby_blocks(const uint64_t* __restrict__ keys, int64_t n, doubl
   }
 }
 
-// per row i: the diagonal entry and sum_j |a_ij| in ascending j (deterministic)
+// per row i: the diagonal entry and sum_j |a_ij| in ascending j (deterministic);
+// off_diagonal: j == i left out, as oracle.cpp's off_diagonal_row_sum does
 __global__ void row_scan_kernel(const int32_t* __restrict__ grid_slot, int32_t dimension,
                                 int32_t nb_logical, const double* __restrict__ payload, int L,
-                                double* __restrict__ diag, double* __restrict__ abs_sum) {
+                                double* __restrict__ diag, double* __restrict__ abs_sum,
+                                bool off_diagonal = false) {
   const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= dimension) return;
   const uint32_t br = static_cast<uint32_t>(i / L);
@@ -94,8 +97,9 @@ __global__ void row_scan_kernel(const int32_t* __restrict__ grid_slot, int32_t d
     const int jn = min(L, dimension - static_cast<int>(bc) * L);
     for (int j = 0; j < jn; ++j) {
       const double v = blk[static_cast<int64_t>(j) * L];
-      s = __dadd_rn(s, fabs(v));
-      if (bc == br && j == r) dv = v;
+      const bool on_diag = bc == br && j == r;
+      if (!(off_diagonal && on_diag)) s = __dadd_rn(s, fabs(v));
+      if (on_diag) dv = v;
     }
   }
   if (diag) diag[i] = dv;
@@ -268,6 +272,36 @@ int spg_matrix_rows(const spg_matrix* m, double* diag, double* abs_row_sums) {
     SPG_CUDA(cudaMemcpyAsync(abs_row_sums, a.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
                              ctx->stream));
   SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  SPG_API_END
+}
+
+int spg_matrix_gershgorin(const spg_matrix* m, double* low, double* high) {
+  SPG_API_BEGIN
+  if (!m || !low || !high) fail(SPG_EINVAL, "null argument");
+  require_payload(m);
+  spg_context* ctx = m->ctx;
+  CtxGuard g(ctx);
+  const int32_t n = m->dimension, nb = (n + m->leaf - 1) / m->leaf;
+  DevBuf<double> d(n, ctx), r(n, ctx);
+  row_scan_kernel<<<grid_for(n, 128), 128, 0, ctx->stream>>>(m->grid_slot, n, nb, m->payload,
+                                                             m->leaf, d.get(), r.get(), true);
+  SPG_CHECK_LAUNCH(ctx);
+  std::vector<double> hd(static_cast<size_t>(n)), hr(static_cast<size_t>(n));
+  SPG_CUDA(cudaMemcpyAsync(hd.data(), d.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaMemcpyAsync(hr.data(), r.get(), n * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  // oracle.cpp:191-200: ascending rows, std::min / std::max semantics
+  double lo = std::numeric_limits<double>::infinity();
+  double hi = -std::numeric_limits<double>::infinity();
+  for (int32_t i = 0; i < n; ++i) {
+    volatile double a = hd[i] - hr[i], b = hd[i] + hr[i];
+    lo = std::min(lo, static_cast<double>(a));
+    hi = std::max(hi, static_cast<double>(b));
+  }
+  *low = lo;
+  *high = hi;
   SPG_API_END
 }
 

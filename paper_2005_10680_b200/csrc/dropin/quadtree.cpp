@@ -5,7 +5,9 @@
 // the reference rule (node_ops.hpp:24-36).  The host Node tree is built only
 // when root() is called, from the downloaded leaves and their device norms;
 // inner norms are recombined on the host with the same sequential rule, so
-// they equal the device pyramid bit for bit.
+// they equal the device pyramid bit for bit.  trace / nnz / scale / add and the
+// Gershgorin bounds run on the device (include/spamm_gpu.h, csrc/algebra.cu):
+// no full-matrix host round trip.
 #include <algorithm>
 #include <cmath>
 #include <stdexcept>
@@ -260,23 +262,6 @@ double QuadTreeMatrix::frobenius_norm() const noexcept {
 }
 
 namespace {
-double node_trace(const NodePtr& n, int size, int leaf) {
-  if (!n) return 0.0;
-  if (n->is_leaf()) {
-    double s = 0.0;
-    for (int i = 0; i < leaf; ++i) s += n->block[i + static_cast<size_t>(i) * leaf];
-    return s;
-  }
-  const int half = size / 2;
-  return node_trace(n->child[0], half, leaf) + node_trace(n->child[3], half, leaf);
-}
-int64_t node_nnz(const NodePtr& n) {
-  if (!n) return 0;
-  if (n->is_leaf()) return std::count_if(n->block.begin(), n->block.end(), [](double v) { return v != 0.0; });
-  int64_t s = 0;
-  for (const NodePtr& c : n->child) s += node_nnz(c);
-  return s;
-}
 void write_dense(const NodePtr& n, DenseMatrix& out, int r0, int c0, int size, int leaf, int limit) {
   if (!n) return;
   if (n->is_leaf()) {
@@ -291,8 +276,22 @@ void write_dense(const NodePtr& n, DenseMatrix& out, int r0, int c0, int size, i
 }
 }  // namespace
 
-double QuadTreeMatrix::trace() const { return node_trace(root(), padded_dimension_, leaf_size_); }
-std::int64_t QuadTreeMatrix::nnz() const { return node_nnz(root()); }
+// node_trace (quadtree.cpp:128-138): per diagonal leaf a sequential sum, then
+// trace(child 0) + trace(child 3) level by level -- spg_matrix_trace
+double QuadTreeMatrix::trace() const {
+  if (!state_) return 0.0;
+  double t = 0.0;
+  b200::check(spg_matrix_trace(device(), &t));
+  return t;
+}
+
+// node_nnz (quadtree.cpp:140-151): stored entries != 0, counted on the device
+std::int64_t QuadTreeMatrix::nnz() const {
+  if (!state_) return 0;
+  int64_t n = 0;
+  b200::check(spg_matrix_nnz(device(), &n));
+  return n;
+}
 
 std::int64_t QuadTreeMatrix::nnz_blocks() const {
   if (!state_) return 0;
@@ -313,50 +312,35 @@ DenseMatrix QuadTreeMatrix::to_dense_padded() const {
   return out;
 }
 
+// scale_node (quadtree.cpp:153-171,249-252): fl(alpha * v) per entry, leaf
+// norms recomputed, all-zero leaves collapse -- spg_matrix_axpby(alpha, a, 0, -)
 QuadTreeMatrix QuadTreeMatrix::scale(double alpha) const {
   if (alpha == 0.0 || !state_) return zero(dimension_, leaf_size_);
-  Leaves lv = download(device(), leaf_size_);
-  for (double& v : lv.payload) v = alpha * v;
-  return adopt_device(upload(lv, dimension_, leaf_size_));
+  spg_matrix* out = nullptr;
+  b200::check(spg_matrix_axpby(b200::context(), alpha, device(), 0.0, nullptr, &out));
+  return adopt_device(out);
 }
 
+// add_nodes (quadtree.cpp:24-36,254-261): a + b where both leaves exist, the
+// present leaf otherwise (fl(1 * v) = v) -- spg_matrix_axpby(1, a, 1, b)
 QuadTreeMatrix add(const QuadTreeMatrix& a, const QuadTreeMatrix& b) {
   if (a.dimension() != b.dimension() || a.leaf_size() != b.leaf_size())
     throw std::invalid_argument("add: dimension or leaf size mismatch");
   if (a.is_zero()) return b;
   if (b.is_zero()) return a;
-  const int L = a.leaf_size();
-  const size_t LL = static_cast<size_t>(L) * L;
-  Leaves la = download(a.device(), L), lb = download(b.device(), L), out;
-  auto key = [](const Leaves& l, size_t i) {
-    return (static_cast<uint64_t>(l.rows[i]) << 32) | static_cast<uint32_t>(l.cols[i]);
-  };
-  std::vector<size_t> ia(la.rows.size()), ib(lb.rows.size());
-  for (size_t i = 0; i < ia.size(); ++i) ia[i] = i;
-  for (size_t i = 0; i < ib.size(); ++i) ib[i] = i;
-  std::sort(ia.begin(), ia.end(), [&](size_t x, size_t y) { return key(la, x) < key(la, y); });
-  std::sort(ib.begin(), ib.end(), [&](size_t x, size_t y) { return key(lb, x) < key(lb, y); });
-  size_t i = 0, j = 0;
-  auto emit = [&](const Leaves& l, size_t k) {
-    out.rows.push_back(l.rows[k]);
-    out.cols.push_back(l.cols[k]);
-    out.payload.insert(out.payload.end(), l.payload.begin() + k * LL, l.payload.begin() + (k + 1) * LL);
-  };
-  while (i < ia.size() || j < ib.size()) {
-    if (j == ib.size() || (i < ia.size() && key(la, ia[i]) < key(lb, ib[j]))) {
-      emit(la, ia[i++]);
-    } else if (i == ia.size() || key(lb, ib[j]) < key(la, ia[i])) {
-      emit(lb, ib[j++]);
-    } else {  // add_nodes leaf case (quadtree.cpp:29-32): a + b elementwise
-      emit(la, ia[i]);
-      double* dst = out.payload.data() + out.payload.size() - LL;
-      const double* src = lb.payload.data() + ib[j] * LL;
-      for (size_t e = 0; e < LL; ++e) dst[e] = dst[e] + src[e];
-      ++i;
-      ++j;
-    }
+  spg_matrix* out = nullptr;
+  b200::check(spg_matrix_axpby(b200::context(), 1.0, a.device(), 1.0, b.device(), &out));
+  return adopt_device(out);
+}
+
+std::pair<double, double> gershgorin_bounds(const QuadTreeMatrix& a) {
+  if (a.is_zero()) {
+    // all diagonal entries and radii are 0 (oracle.cpp:191-200 on a zero matrix)
+    return {0.0, 0.0};
   }
-  return adopt_device(upload(out, a.dimension(), L));
+  double lo = 0.0, hi = 0.0;
+  b200::check(spg_matrix_gershgorin(a.device(), &lo, &hi));
+  return {lo, hi};
 }
 
 }  // namespace spamm

@@ -773,9 +773,13 @@ int spg_matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf
   *out = nullptr;
   if (n_leaves < 0) fail(SPG_EINVAL, "negative leaf count");
   if (n_leaves && (!block_rows || !block_cols || !norms)) fail(SPG_EINVAL, "null argument");
+  // (row, col) strictly ascending: panel plans (spg_matrix_gather_rows emits
+  // (row, col) order) pair B slots with this table's order
   for (int64_t t = 1; t < n_leaves; ++t)
-    if (block_rows[t] < block_rows[t - 1])
-      fail(SPG_EINVAL, "leaf norms: leaves must be sorted by block row");
+    if (block_rows[t] < block_rows[t - 1] ||
+        (block_rows[t] == block_rows[t - 1] && block_cols[t] <= block_cols[t - 1]))
+      fail(SPG_EINVAL, "leaf norms: leaves must be sorted by (block row, block col) without "
+                       "duplicates");
   int32_t padded = 0, depth = 0;
   check_shape(dimension, leaf_size, &padded, &depth);
   CtxGuard g(ctx);

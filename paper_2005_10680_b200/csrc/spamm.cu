@@ -53,14 +53,16 @@ __global__ void run_outputs(const uint64_t* __restrict__ keys, const int64_t* __
 
 __global__ void make_pairs(const uint64_t* __restrict__ keys, int64_t n, int kbits,
                            const int32_t* __restrict__ gridA, const int32_t* __restrict__ gridB,
-                           int2* __restrict__ pairs) {
+                           int2* __restrict__ pairs, int* __restrict__ missing = nullptr) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const uint64_t key = keys[t];
   const uint32_t k = static_cast<uint32_t>(key & ((uint64_t(1) << kbits) - 1));
   const uint64_t ij = key >> kbits;
   const uint32_t i = morton_row(ij), j = morton_col(ij);
-  pairs[t] = make_int2(gridA[morton2(i, k)], gridB[morton2(k, j)]);
+  const int2 p = make_int2(gridA[morton2(i, k)], gridB[morton2(k, j)]);
+  pairs[t] = p;
+  if (missing && (p.x < 0 || p.y < 0)) *missing = 1;
 }
 
 // leaves of a matrix per block column (use_col) or row; with use_col, only
@@ -507,10 +509,25 @@ Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
         pl.out_offset.get());
     SPG_CHECK_LAUNCH(ctx);
     pl.pairs = DevBuf<int2>(n_surv, ctx);
+    // norms and payload slots from different matrices (a_norms plans): a
+    // survivor whose A leaf the slot matrix lacks would read A + (-1) L^2
+    const bool split = a_slots != a;
+    DevBuf<int> missing(split ? 1 : 0, ctx);
+    if (split) SPG_CUDA(cudaMemsetAsync(missing.get(), 0, sizeof(int), ctx->stream));
     make_pairs<<<grid_for(n_surv, 256), 256, 0, ctx->stream>>>(tl.keys.get(), n_surv, tl.kbits,
                                                               a_slots->grid_slot, b->grid_slot,
-                                                              pl.pairs.get());
+                                                              pl.pairs.get(),
+                                                              split ? missing.get() : nullptr);
     SPG_CHECK_LAUNCH(ctx);
+    if (split) {
+      int h = 0;
+      SPG_CUDA(cudaMemcpyAsync(&h, missing.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h)
+        fail(SPG_EINVAL, "plan: a_norms lists a leaf in the shard rows that the local A does "
+                         "not hold (the shard rows of a and a_norms must have the same leaves)");
+    }
   }
   if (keep_keys) pl.keys = std::move(tl.keys);
   return pl;

@@ -1,13 +1,19 @@
 // test_experiment.cpp -- the drop-in's experiment-side modules (SURVEY 8f row
-// 4: MatrixMarket I/O, the decay-model generator and dense helpers, the
-// squaring / purification runners and RunRecord CSV / JSON output) against
-// the reference itself, loaded from oracle/_ref/libspamm_ref.so (the
-// unmodified reference sources, namespace-renamed, with C entry points in
-// oracle/ref_adapter.cpp).
+// 4: MatrixMarket I/O, the squaring / purification runners, device Gershgorin
+// bounds and RunRecord CSV / JSON output) against the reference itself,
+// loaded from oracle/_ref/libspamm_ref.so (the unmodified reference sources,
+// namespace-renamed, with C entry points in oracle/ref_adapter.cpp).
 //
-//   test_experiment host OUTDIR   -- no GPU: generator, bounds, density
-//                                    oracle, MatrixMarket reading, emit
-//   test_experiment gpu OUTDIR    -- experiments and MatrixMarket writing
+// The reference's dense test helpers (spamm::oracle::generate_decay_matrix,
+// density_matrix_oracle) are NOT in the product library: this program links
+// oracle/_ref/libspamm_dense_oracle.so (the unmodified src/oracle.cpp) and
+// registers them with spamm::set_experiment_oracle, as a reference caller
+// (the CLI) would.
+//
+//   test_experiment host OUTDIR   -- no GPU: the linked dense oracle is the
+//                                    reference's, MatrixMarket reading, emit,
+//                                    the unregistered-generator error
+//   test_experiment gpu OUTDIR    -- experiments, Gershgorin, MatrixMarket writing
 #include <dlfcn.h>
 
 #include <cmath>
@@ -90,6 +96,7 @@ static int our_status(const std::function<void()>& fn) {
 }
 
 // ---- host-side cases --------------------------------------------------------
+// the linked dense oracle is the reference's (same bits as libspamm_ref's copy)
 static void test_generator(const Ref& ref) {
   g_case = "generate_decay_matrix";
   struct P {
@@ -116,15 +123,56 @@ static void test_generator(const Ref& ref) {
     CHECK(so == sr);
     if (so == 0 && sr == 0) {
       CHECK(bits_equal(ours.data(), theirs.data(), ours.size()));
-      double lo = 0, hi = 0;
-      ref.gershgorin(theirs.data(), p.n, &lo, &hi);
-      const auto b = oracle::gershgorin_bounds(ours);
-      CHECK(b.first == lo && b.second == hi);
-      CHECK(b.first >= p.lo - 1e-12 && b.second <= p.hi + 1e-12);
     }
   }
 }
 
+// a generated-input config with no generator registered fails loudly
+static void test_unregistered_generator() {
+  g_case = "unregistered generator";
+  set_experiment_oracle({});
+  ExperimentConfig cfg;
+  cfg.generated = oracle::DecayModelSpec{};
+  cfg.generated->dimension = 8;
+  cfg.tolerances = {1e-3};
+  bool threw = false;
+  try {
+    run_squaring_experiment(cfg);
+  } catch (const std::logic_error& e) {
+    threw = std::string(e.what()).find("set_experiment_oracle") != std::string::npos;
+  }
+  CHECK(threw);
+}
+
+// spamm::gershgorin_bounds on the device leaves == the reference's dense
+// oracle::gershgorin_bounds (oracle.cpp:191-200), bit for bit
+static void test_gershgorin(const Ref& ref) {
+  g_case = "gershgorin_bounds";
+  struct P {
+    int n, leaf;
+    double alpha, scale, lo, hi;
+    std::uint64_t seed;
+  };
+  const P cases[] = {{1, 4, 0.5, 0.3, 0.0, 2.0, 0}, {37, 4, 0.5, 0.3, 0.0, 2.0, 7},
+                     {200, 16, 0.2, 0.1, -1.0, 1.0, 123456789}, {64, 32, 1.5, 0.9, -3.0, 3.0, 42}};
+  for (const P& p : cases) {
+    oracle::DecayModelSpec spec;
+    spec.dimension = p.n;
+    spec.alpha = p.alpha;
+    spec.scale = p.scale;
+    spec.spectral_low = p.lo;
+    spec.spectral_high = p.hi;
+    spec.seed = p.seed;
+    DenseMatrix d = oracle::generate_decay_matrix(spec);
+    for (std::size_t i = 3; i < d.size(); i += 11) d.data()[i] = 0.0;  // ragged sparsity
+    double lo = 0, hi = 0;
+    ref.gershgorin(d.data(), p.n, &lo, &hi);
+    const auto b = gershgorin_bounds(QuadTreeMatrix::from_dense(d, p.leaf));
+    CHECK(b.first == lo && b.second == hi);
+  }
+}
+
+// the linked dense oracle is the reference's (same bits as libspamm_ref's copy)
 static void test_density_oracle(const Ref& ref) {
   g_case = "density_matrix_oracle";
   oracle::DecayModelSpec spec;
@@ -377,11 +425,15 @@ int main(int argc, char** argv) {
   }
   try {
     if (mode == "host") {
+      test_unregistered_generator();
+      set_experiment_oracle({&oracle::generate_decay_matrix, &oracle::density_matrix_oracle});
       test_generator(ref);
       test_density_oracle(ref);
       test_mm_read(ref);
       test_emit(outdir);
     } else {
+      set_experiment_oracle({&oracle::generate_decay_matrix, &oracle::density_matrix_oracle});
+      test_gershgorin(ref);
       test_mm_write(ref, outdir);
       test_squaring(ref, outdir);
       test_purification(outdir);

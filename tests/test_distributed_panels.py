@@ -144,6 +144,24 @@ def test_plan_contract_errors(ctx):
     with pytest.raises(ValueError):  # unsorted leaf table
         r, c, nr = leaf_table(B)
         nat.from_leaf_norms(ctx, n, L, r[::-1], c[::-1], nr[::-1])
+    r, c, nr = leaf_table(B)
+    row0 = np.flatnonzero(r == r[0])
+    assert len(row0) > 1
+    with pytest.raises(ValueError):  # rows sorted, columns not (gather_rows pairs by order)
+        sw = np.arange(len(r))
+        sw[row0[0]], sw[row0[1]] = row0[1], row0[0]
+        nat.from_leaf_norms(ctx, n, L, r[sw], c[sw], nr[sw])
+    with pytest.raises(ValueError):  # duplicate leaf
+        nat.from_leaf_norms(ctx, n, L, np.r_[r[:1], r], np.r_[c[:1], c], np.r_[nr[:1], nr])
+    # a_norms listing a shard-row leaf the local A lacks: refused, no wild read
+    An = nat.from_leaf_norms(ctx, n, L, *leaf_table(A))
+    ra, ca, pa, _ = As[0].download()
+    keep = np.ones(len(ra), bool)
+    keep[len(ra) // 2] = False
+    A_hole = nat.upload(ctx, n, L, ra[keep], ca[keep], pa[keep])
+    with pytest.raises(ValueError, match="a_norms"):
+        nat.Plan(ctx, A_hole, Bn, 0.0, 1, 0, a_norms=An)
+    nat.Plan(ctx, As[0], Bn, 0.0, 1, 0, a_norms=An)  # the consistent shard is accepted
 
 
 @pytest.mark.gpu

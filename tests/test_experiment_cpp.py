@@ -14,18 +14,24 @@ from conftest import ROOT
 
 BIN = ROOT / "tests" / "cpp" / "bin" / "test_experiment"
 LIB = ROOT / "paper_2005_10680_b200" / "lib"
+# the reference's own src/oracle.cpp (dense test helpers), built by oracle/Makefile
+DENSE = ROOT / "oracle" / "_ref" / "libspamm_dense_oracle.so"
 REF = ROOT / "oracle" / "_ref" / "libspamm_ref.so"
 
 
 def compile_test():
+    if not DENSE.exists():
+        pytest.skip("oracle/_ref/libspamm_dense_oracle.so (reference dense helpers) not built")
     BIN.parent.mkdir(parents=True, exist_ok=True)
     src = ROOT / "tests" / "cpp" / "test_experiment.cpp"
     if BIN.exists() and BIN.stat().st_mtime > max(src.stat().st_mtime,
-                                                  (LIB / "libspamm_ec.so").stat().st_mtime):
+                                                  (LIB / "libspamm_ec.so").stat().st_mtime,
+                                                  DENSE.stat().st_mtime):
         return BIN
     subprocess.run(["g++", "-std=c++20", "-O2", "-ffp-contract=off", f"-I{ROOT / 'include'}",
                     str(src), "-o", str(BIN), f"-L{LIB}", "-lspamm_ec", "-lspamm_gpu", "-ldl",
-                    f"-Wl,-rpath,{LIB}"], check=True)
+                    f"-Wl,-rpath,{LIB}", f"-L{DENSE.parent}", "-lspamm_dense_oracle",
+                    f"-Wl,-rpath,{DENSE.parent}"], check=True)
     return BIN
 
 

@@ -193,3 +193,65 @@ def test_row_data_and_diagonal_matrices(ctx):
     D = nat.from_diagonal(ctx, v, L)
     assert np.array_equal(D.to_dense(), np.diag(v))
     assert nat.trace(D) == pytest.approx(v.sum(), rel=1e-14)
+
+
+def test_gershgorin_bounds_match_reference(ctx):
+    """spg_matrix_gershgorin (device row scan, j != i) equals the reference's
+    oracle::gershgorin_bounds on the dense matrix bit for bit
+    (oracle.cpp:191-200), ragged last block and empty block columns included."""
+    import ctypes
+    import oracle
+    from paper_2005_10680_b200 import _native as nat
+    if not oracle.available("ref"):
+        pytest.skip("reference build (oracle/_ref) not present")
+    R = oracle.Oracle("ref")
+    f = R.L.ref_gershgorin
+    f.restype = None
+    f.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    rng = np.random.default_rng(9)
+    for n, L in ((333, 16), (64, 64), (1000, 32)):
+        d = np.where(rng.uniform(size=(n, n)) < 0.3, rng.uniform(-1, 1, (n, n)), 0.0)
+        d = d + d.T + np.diag(rng.uniform(-3, 3, n))
+        d[:, n // 3:n // 3 + 20] = 0.0
+        d = np.ascontiguousarray(d)
+        lo, hi = ctypes.c_double(), ctypes.c_double()
+        f(d.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n, ctypes.byref(lo),
+          ctypes.byref(hi))
+        got = nat.gershgorin(nat.from_dense(ctx, d, L))
+        assert got == (lo.value, hi.value)
+
+
+def test_device_algebra_matches_reference_build(ctx):
+    """trace / nnz / scale / add on the device (spg_matrix_trace, _nnz, _axpby:
+    what the drop-in's QuadTreeMatrix::trace/nnz/scale and spamm::add call)
+    against the reference build's own QuadTreeMatrix methods (quadtree.cpp:
+    231-261): trace bitwise, nnz exact, every leaf's payload and norm bitwise,
+    the same null leaves (zero-collapse included)."""
+    import oracle
+    from paper_2005_10680_b200 import _native as nat
+    if not oracle.available("ref"):
+        pytest.skip("reference build (oracle/_ref) not present")
+    R = oracle.Oracle("ref")
+    rng = np.random.default_rng(21)
+    for n, L in ((333, 16), (256, 32), (100, 8)):
+        a = np.where(rng.uniform(size=(n, n)) < 0.2, rng.uniform(-1, 1, (n, n)), 0.0)
+        b = np.where(rng.uniform(size=(n, n)) < 0.2, rng.uniform(-1, 1, (n, n)), 0.0)
+        b[: n // 2, : n // 2] = -a[: n // 2, : n // 2]  # a + b cancels -> leaves collapse
+        b[n // 2:, :] = 0.0
+        A, B = nat.from_dense(ctx, a, L), nat.from_dense(ctx, b, L)
+        r, c, p, _ = A.download()
+        RA = R.build(n, L, r, c, p)
+        r, c, p, _ = B.download()
+        RB = R.build(n, L, r, c, p)
+        assert nat.trace(A) == R.trace(RA)
+        assert nat.nnz(A) == R.nnz(RA)
+        for alpha, beta, use_b in ((1.0, 1.0, True), (2.5, -0.75, True), (-1.0, 0.0, False),
+                                   (1e-300, 0.0, False)):
+            got = nat.axpby(ctx, alpha, A, beta, B) if use_b else nat.axpby(ctx, alpha, A)
+            want = R.axpby(alpha, RA, beta, RB if use_b else None)
+            gr, gc, gp, gn = got.download()
+            wr, wc, wp, wn = want.leaves()
+            assert np.array_equal(gr, wr) and np.array_equal(gc, wc)
+            assert gp.tobytes() == wp.tobytes() and gn.tobytes() == wn.tobytes()
+            assert nat.trace(got) == R.trace(want) and nat.nnz(got) == R.nnz(want)
