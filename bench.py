@@ -68,8 +68,9 @@ def parse():
                         "memory by one GEMM (CUDA IPC / NVLink; every L2 miss crosses the link)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-rows", type=int, default=4,
-                   help="block-rows of A in the bounded CPU sample")
+    p.add_argument("--cpu-rows", type=int, default=1,
+                   help="block rows per fork-join row group in the bounded CPU sample "
+                        "(sample_rows)")
     return p.parse_args()
 
 
@@ -131,6 +132,41 @@ class Dist:
         parts = [torch.empty_like(t) for _ in range(self.world)]
         self.pg.all_gather(parts, t)
         return torch.stack(parts).numpy()
+
+    def all_gather_arrays(self, arrays):
+        """Per-rank lists of numpy arrays (any dtype, per-rank lengths) ->
+        [rank][i] on every rank, through device-buffer collectives (NCCL
+        all_gather_into_tensor on the GPUs; gloo on CPU): the byte counts
+        first, then one padded byte buffer per array.  Replaces pickling with
+        all_gather_object (leaf-norm tables are ~200 MB per rank on config 4)."""
+        if not self.pg:
+            return [list(arrays)]
+        import torch
+        dev = self._dev()
+        flat = [np.ascontiguousarray(a) for a in arrays]
+        nbytes = torch.tensor([a.nbytes for a in flat], dtype=torch.int64, device=dev)
+        sizes = self._gather(nbytes).cpu().numpy()  # (world, n_arrays)
+        out = [[None] * len(flat) for _ in range(self.world)]
+        for i, a in enumerate(flat):
+            width = max(int(sizes[:, i].max()), 1)
+            buf = torch.zeros(width, dtype=torch.uint8, device=dev)
+            if a.nbytes:
+                buf[:a.nbytes] = torch.from_numpy(a.reshape(-1).view(np.uint8)).to(dev)
+            host = self._gather(buf).cpu().numpy()
+            for r in range(self.world):
+                v = host[r, :int(sizes[r, i])].view(a.dtype)
+                out[r][i] = v.reshape((-1,) + a.shape[1:]).copy()
+        return out
+
+    def _gather(self, t):
+        if self.backend == "nccl":
+            out = t.new_empty((self.world,) + tuple(t.shape))
+            self.pg.all_gather_into_tensor(out, t)
+            return out
+        parts = [t.new_empty(t.shape) for _ in range(self.world)]
+        self.pg.all_gather(parts, t)
+        import torch
+        return torch.stack(parts)
 
     def close(self):
         if self.pg:
@@ -195,25 +231,85 @@ def make_matrix(nat, ctx, w):
     return nat.synth_chain_device(ctx, w.n, w.leaf, w.ell, w.value_seed, w.drop)
 
 
-def cpu_sample(kind, rows, cols, pay, w, taus, tau_star, sample_rows, threads):
-    """The reference CPU implementation on a bounded slice of the workload:
-    spamm_with_error_control's two phases -- cse(A_rows, A) and
-    spamm_multiply(A_rows, A, tau*) -- for the first `sample_rows` block-rows of
-    A (A_rows = A restricted to those rows, B = the full A), with tau* the
-    full problem's selected tolerance.  Returns (tflops, seconds, flops)."""
-    import oracle
-    R = oracle.Oracle(kind)
-    R.set_threads(threads)
-    full = R.build(w.n, w.leaf, rows, cols, pay)
-    sel = rows < sample_rows
-    part = R.build(w.n, w.leaf, rows[sel], cols[sel], pay[sel])
-    surv = len(R.survivors(part, full, tau_star))
-    flops = 2.0 * w.leaf ** 3 * surv
-    t0 = time.perf_counter()
-    R.cse(part, full, taus)
-    R.spamm(part, full, tau_star)
-    dt = time.perf_counter() - t0
-    return flops / dt / 1e12, dt, flops, surv
+def spawn_levels(threads: int) -> int:
+    """The reference's fork-join depth (execution.cpp:17-23): 4^levels tasks."""
+    levels, cap = 0, 1
+    while cap < threads and levels < 3:
+        cap *= 4
+        levels += 1
+    return levels
+
+
+def sample_rows(nb: int, threads: int, per_group: int = 1):
+    """Block rows of the bounded CPU sample, spread so that every task the
+    reference spawns has work: spawn_levels(threads) levels of 4-way spawning
+    split C into 2^levels x 2^levels output quadrants (multiply.cpp:79-84,
+    error_control.cpp:59-66), so `per_group` rows in each of the 2^levels row
+    groups give every quadrant task a row (e.g. rows 0,128,256,384 of 512 for
+    16 threads)."""
+    groups = 1 << spawn_levels(threads)
+    padded = 1 << max(0, (nb - 1).bit_length())
+    per = max(padded // groups, 1)
+    return sorted({g * per + o for g in range(groups) for o in range(per_group)
+                   if o < per and g * per + o < nb})
+
+
+class ReferenceSample:
+    """The reference CPU implementation (oracle/_ref: the unmodified reference
+    sources; `port` = the C restatement when the reference is not built) on
+    the workload: its own cse over the FULL matrices picks tau* (the
+    reference's tau-sweep, timed whole), and spamm_multiply runs on a bounded
+    sample of block rows (A_rows * B, exactly those rows of C~: same leaf
+    decisions, same per-block k order), timed and scaled by the survivor
+    counts to the full product.  One step estimate =
+        t_cse(full) + t_spamm(sample) * S(tau*) / S_sample(tau*)
+    and value = 2 L^3 S(tau*) / step estimate.  Mirrors
+    spamm_with_error_control's two timed phases (error_control.cpp:207-217)."""
+
+    def __init__(self, w, rows, cols, pay, taus, threads, per_group=1):
+        import oracle
+        self.kind = "ref" if oracle.available("ref") else "port"
+        self.threads = threads if self.kind == "ref" else 1
+        R = oracle.Oracle(self.kind)
+        R.set_threads(self.threads)
+        self.R, self.w, self.taus = R, w, taus
+        self.full = R.build(w.n, w.leaf, rows, cols, pay)
+        nb = -(-w.n // w.leaf)
+        self.rows = sample_rows(nb, self.threads, per_group)
+        sel = np.isin(rows, self.rows)
+        self.part = R.build(w.n, w.leaf, rows[sel], cols[sel], pay[sel])
+        self.tau = None
+
+    def step(self):
+        """(t_cse, t_spamm_sample, bounds): one timed cse + sampled spamm."""
+        t0 = time.perf_counter()
+        bounds = self.R.cse(self.full, self.full, self.taus)
+        t_cse = time.perf_counter() - t0
+        k = next((i for i, b in enumerate(bounds) if b < self.w.delta), -1)
+        tau = float(self.taus[k]) if k >= 0 else 0.0
+        if self.tau is None:  # survivor counts at the reference's own tau*
+            self.tau, self.k = tau, k
+            self.s_total = int(self.R._surv(self.full.h, self.full.h, tau, None, 0))
+            self.s_sample = int(self.R._surv(self.part.h, self.full.h, tau, None, 0))
+        t0 = time.perf_counter()
+        self.R.spamm(self.part, self.full, tau)
+        t_spamm = time.perf_counter() - t0
+        return t_cse, t_spamm, bounds
+
+    def estimate(self, t_cse, t_spamm):
+        scale = self.s_total / max(self.s_sample, 1)
+        step_s = t_cse + t_spamm * scale
+        flops = 2.0 * self.w.leaf ** 3 * self.s_total
+        return flops / step_s / 1e12, step_s, flops
+
+    def describe(self, t_cse, t_spamm):
+        return (f"{self.w.name}: reference cse(A, A) over the full matrix (tau*={self.tau:.4g}, "
+                f"k={self.k}) + spamm_multiply(A_rows, A, tau*) on block rows "
+                f"{self.rows} of {-(-self.w.n // self.w.leaf)} ({self.s_sample} of "
+                f"{self.s_total} leaf products), scaled by S/S_sample = "
+                f"{self.s_total / max(self.s_sample, 1):.1f}; fork-join on {self.threads} "
+                f"threads ({4 ** spawn_levels(self.threads)} tasks, each with work); "
+                f"t_cse {t_cse:.3f} s, t_spamm(sample) {t_spamm:.3f} s")
 
 
 def ncu_entry(key):
@@ -259,13 +355,8 @@ def run_ours(args, dist):
         else:
             A = nat.synth_chain_device_rows(ctx, w.n, w.leaf, w.ell, w.value_seed, w.drop, lo, hi)
 
-        def allgather(arrays):
-            if dist.world == 1:
-                return [arrays]
-            out = [None] * dist.world
-            dist.pg.all_gather_object(out, arrays)
-            return out
-        ops = DistributedOperands(ctx, A, A, level, dist.rank, allgather, args.transport)
+        ops = DistributedOperands(ctx, A, A, level, dist.rank, dist.all_gather_arrays,
+                                  args.transport)
         fetch = torch_fetch(dist.backend or "none", dist.rank, A, w.leaf)
     else:
         A = make_matrix(nat, ctx, w)
@@ -504,84 +595,103 @@ def run_e2e(args, nat, ctx, stream, A, w, taus):
 
 
 def run_cpu_baseline(args, nat, A, w, taus, tau_star, host=None):
-    import oracle
+    """The reference beside the GPU arm (rank 0, N = 1): one ReferenceSample
+    step on the same input bits (downloaded from the device)."""
     if host is None:
         rows, cols, pay, _ = A.download(payload=True)
     else:
         rows, cols, pay = host
-    kind = "ref" if oracle.available("ref") else "port"
     threads = os.cpu_count() or 1
-    tf, dt, flops, surv = cpu_sample(kind, rows, cols, pay, w, taus, tau_star, args.cpu_rows,
-                                     threads)
-    return {"value": tf, "unit": "TFLOP/s", "cores": threads if kind == "ref" else 1,
-            "kind": "reference" if kind == "ref" else "port",
-            "seconds": round(dt, 3),
-            "sample": f"{w.name}: cse(A_rows, A) + spamm_multiply(A_rows, A, tau*={tau_star:.4g}) "
-                      f"for block-rows [0,{args.cpu_rows}) of {w.n // w.leaf} "
-                      f"({surv} leaf products, {flops / 1e9:.1f} GFLOP)"}
+    ref = ReferenceSample(w, rows, cols, pay, taus, threads, args.cpu_rows)
+    t_cse, t_spamm, _ = ref.step()
+    tf, step_s, _ = ref.estimate(t_cse, t_spamm)
+    return {"value": tf, "unit": "TFLOP/s", "cores": ref.threads,
+            "kind": "reference" if ref.kind == "ref" else "port",
+            "step_seconds_estimate": round(step_s, 3), "seconds_cse": round(t_cse, 3),
+            "seconds_spamm_sample": round(t_spamm, 3),
+            "tau_matches_gpu": ref.tau == tau_star,
+            "sample": ref.describe(t_cse, t_spamm)}
 
 
 def run_reference(args, dist):
     """--impl reference: the reference's own CPU implementation (oracle/_ref,
-    unmodified reference sources) on the same workload/metric, all host
-    threads, each step a bounded sample.  Rank 0 only."""
+    unmodified reference sources) on the same workload / metric with all host
+    threads: each step = its full cse + a sampled spamm_multiply scaled to the
+    full product (ReferenceSample).  The input comes from the host generator in
+    oracle/ (bitwise the product's host generator; the GPU arm's device
+    generator differs from it only through exp()) -- the product library is
+    never loaded.  Rank 0 only."""
     if dist.rank != 0:
         return None
-    from paper_2005_10680_b200 import _native as nat
-    from paper_2005_10680_b200.inputs import CONFIGS, log_grid
+    from paper_2005_10680_b200.inputs import CONFIGS, log_grid  # pure Python
     import oracle
     w = CONFIGS[args.workload]
-    # Input generation (not timed, not on the measured path): the same seeded
-    # matrix bits the GPU arm uses, produced by the device generator.
-    ctx = nat.Context(dist.device)
-    A = make_matrix(nat, ctx, w)
-    taus = log_grid(w.n_taus)
-    rows, cols, pay, _ = A.download(payload=True)
-    bounds = nat.cse(ctx, A, A, taus)
-    tau_star, _ = nat.select_tolerance(bounds, taus, w.delta)
-    del A
-    ctx.close()
-    kind = "ref" if oracle.available("ref") else "port"
     threads = os.cpu_count() or 1
-    R = oracle.Oracle(kind)
-    R.set_threads(threads)
-    full = R.build(w.n, w.leaf, rows, cols, pay)
-    sel = rows < args.cpu_rows
-    part = R.build(w.n, w.leaf, rows[sel], cols[sel], pay[sel])
-    surv = len(R.survivors(part, full, tau_star))
-    flops = 2.0 * w.leaf ** 3 * surv
+    t0 = time.perf_counter()
+    rows, cols, pay = oracle.host_inputs(w, threads)
+    t_gen = time.perf_counter() - t0
+    taus = log_grid(w.n_taus)
+    ref = ReferenceSample(w, rows, cols, pay, taus, threads, args.cpu_rows)
+    del rows, cols, pay
     for _ in range(min(args.warmup, 1)):
-        R.cse(part, full, taus)
-        R.spamm(part, full, tau_star)
-    times = []
+        ref.step()
+    cses, spamms = [], []
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        R.cse(part, full, taus)
-        R.spamm(part, full, tau_star)
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
-    value = flops * args.steps / total / 1e12
-    sample = (f"{w.name}: cse(A_rows, A) + spamm_multiply(A_rows, A, tau*={tau_star:.4g}) for "
-              f"block-rows [0,{args.cpu_rows}) of {w.n // w.leaf} ({surv} leaf products)")
+        t_cse, t_spamm, _ = ref.step()
+        cses.append(t_cse)
+        spamms.append(t_spamm)
+    t_cse, t_spamm = sum(cses) / len(cses), sum(spamms) / len(spamms)
+    value, step_s, flops = ref.estimate(t_cse, t_spamm)
+    sample = ref.describe(t_cse, t_spamm)
     return {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "ms_per_step": round(1e3 * step_s, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: seeded 3-D cluster decay matrix (DESIGN.md Inputs)",
-        "config": {"workload": w.name, "n": w.n, "leaf": w.leaf, "delta": w.delta,
-                   "n_taus": w.n_taus},
+        "data": (f"synthetic: seeded {'3-D cluster' if w.kind == 'cluster' else '1-D chain'} "
+                 f"decay matrix (DESIGN.md Inputs), host generator (oracle/libinputs.so, "
+                 f"{t_gen:.1f} s)"),
+        "config": {"workload": w.name, "n": w.n, "leaf": w.leaf, "ell": w.ell,
+                   "density": w.density, "delta": w.delta, "n_taus": w.n_taus,
+                   "tau_grid": "log-spaced [1e-12, 1e-2]", "drop": w.drop},
         "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "TFLOP/s",
-                         "cores": threads if kind == "ref" else 1,
-                         "kind": "reference" if kind == "ref" else "port", "sample": sample},
+        "tau": ref.tau, "tau_index": ref.k, "survivors": ref.s_total,
+        "sweep_ms": round(1e3 * t_cse, 3),
+        "phase_s": {"cse": round(t_cse, 3), "spamm_sample": round(t_spamm, 3),
+                    "spamm_full_estimate": round(step_s - t_cse, 3)},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": ref.threads,
+                         "kind": "reference" if ref.kind == "ref" else "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
 
 
+def launch_ranks(n: int) -> int:
+    """`--gpus N` without a torch.distributed launcher: start the N ranks
+    ourselves, one process per GPU, exactly as the driver's torchrun command
+    would (127.0.0.1 rendezvous), and return the launcher's exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator set-up (transport, NVLS) on stderr
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args.gpus))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     dist = Dist()
     try:
         if args.impl == "reference":

@@ -251,6 +251,41 @@ class Oracle:
         return out
 
 
+INPUTS_LIB = HERE / "libinputs.so"
+
+
+def host_inputs(w, threads: int | None = None, value_seed: int | None = None):
+    """(rows, cols, payload) of BASELINE workload `w` (inputs.Workload) from
+    oracle/libinputs.so: bitwise the product's host generator
+    (spg_synth_*_host), multi-threaded, without loading the product library."""
+    import os
+    L = C.CDLL(str(INPUTS_LIB))
+    threads = threads or os.cpu_count() or 1
+    seed = w.value_seed if value_seed is None else value_seed
+    nb = -(-w.n // w.leaf)
+    cap = nb * nb
+    rows = np.empty(cap, np.int32)
+    cols = np.empty(cap, np.int32)
+    pay = np.empty((cap, w.leaf * w.leaf))
+    n = C.c_int64(0)
+    if w.kind == "cluster":
+        f = L.inp_cluster
+        f.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, C.c_uint64,
+                      C.c_double, C.c_int, C.c_int64, _i32p, _i32p, _dp, C.POINTER(C.c_int64)]
+        rc = f(w.n, w.leaf, w.ell, w.density, w.site_seed, seed, w.drop, threads, cap,
+               _p(rows, C.c_int32), _p(cols, C.c_int32), _p(pay, C.c_double), C.byref(n))
+    else:
+        f = L.inp_chain
+        f.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double, C.c_int,
+                      C.c_int64, _i32p, _i32p, _dp, C.POINTER(C.c_int64)]
+        rc = f(w.n, w.leaf, w.ell, seed, w.drop, threads, cap, _p(rows, C.c_int32),
+               _p(cols, C.c_int32), _p(pay, C.c_double), C.byref(n))
+    if rc != 0:
+        raise ValueError("host_inputs: invalid workload")
+    k = n.value
+    return rows[:k], cols[:k], pay[:k]
+
+
 def leaves_to_dense(n: int, leaf: int, rows, cols, payload) -> np.ndarray:
     nb = (n + leaf - 1) // leaf
     pad = np.zeros((nb * leaf, nb * leaf))
