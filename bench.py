@@ -646,7 +646,10 @@ def run_reference(args, dist):
     return {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * step_s, 3), "higher_is_better": True,
+        # measured wall time of one timed step (full cse + the sampled spamm);
+        # value is the full product's throughput estimated from it
+        "ms_per_step": round(1e3 * (t_cse + t_spamm), 3),
+        "full_step_estimate_ms": round(1e3 * step_s, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": (f"synthetic: seeded {'3-D cluster' if w.kind == 'cluster' else '1-D chain'} "
                  f"decay matrix (DESIGN.md Inputs), host generator (oracle/libinputs.so, "
