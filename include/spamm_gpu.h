@@ -170,6 +170,16 @@ int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
 int spg_survivors(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                   int64_t* count, int32_t* triples, int64_t capacity);
 
+/* Survivor-set digest of A*B at tau restricted to the output block rows of
+ * shard `shard` of 2^level (level 0: the whole product), from the product's
+ * own task-list builder: count and sum over the surviving (i, k, j) of
+ * mix64(i << 42 | k << 21 | j) mod 2^64 (mix64 = SplitMix64 finaliser).  The
+ * sum is order-free and additive over disjoint shards, so per-shard digests
+ * of a sharded run add up to the whole product's -- the form in which the
+ * survivor SET is pinned against the reference at configs 2-5 sizes. */
+int spg_survivor_digest(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                        int32_t level, int32_t shard, int64_t* count, uint64_t* digest);
+
 /* Parity audit: of all candidate leaf products (non-null
  * A(i,k) x B(k,j)), how many have |fl(nA*nB) - tau| <= ulps * ulp(tau) --
  * the decisions a one-ulp norm difference could flip. */

@@ -127,6 +127,9 @@ class Oracle:
             self._trace = fn("trace", C.c_double, [_vp])
             self._nnz_entries = fn("nnz", C.c_int64, [_vp])
             self._axpby = fn("axpby", _vp, [C.c_double, _vp, C.c_double, _vp])
+            self._digest = fn("survivor_digest", None, [_vp, _vp, C.c_double, C.c_int,
+                                                        C.POINTER(C.c_int64),
+                                                        C.POINTER(C.c_uint64)])
             self._purify = fn("purify", _vp, [_vp, C.c_int, C.c_int, C.c_int, C.c_double, _dp,
                                               C.c_int, C.c_double, _dp, C.c_double, C.c_int,
                                               C.POINTER(C.c_int), _dp, C.POINTER(C.c_int),
@@ -168,6 +171,14 @@ class Oracle:
         if not h:
             raise ValueError("axpby: invalid arguments")
         return Tree(self, h, a.leaf)
+
+    def survivor_digest(self, a: Tree, b: Tree, tau: float, threads: int = 0):
+        """(count, digest) of spamm_multiply(a, b, tau)'s survivor set; the same
+        function of the set as spg_survivor_digest (ref back end only)."""
+        import os
+        n, d = C.c_int64(0), C.c_uint64(0)
+        self._digest(a.h, b.h, tau, threads or os.cpu_count() or 1, C.byref(n), C.byref(d))
+        return n.value, d.value
 
     def set_threads(self, n: int):
         if self.kind == "ref":

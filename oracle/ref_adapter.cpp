@@ -14,6 +14,8 @@
 #include <exception>
 #include <memory>
 #include <vector>
+#include <thread>
+#include <atomic>
 
 #include "node_ops.hpp"
 #include <sstream>
@@ -166,9 +168,85 @@ void surv_walk(const NodePtr& a, const NodePtr& b, int level, int depth, double 
                   2 * I + row, 2 * K + h, 2 * J + col, out, count);
 }
 
+std::uint64_t digest_mix(std::uint64_t z) {  // SplitMix64 finaliser (spg_survivor_digest)
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// spamm_node's decisions (multiply.cpp:70-92) on reference trees, reduced to
+// (count, sum of digest_mix(i << 42 | k << 21 | j))
+void digest_walk(const NodePtr& a, const NodePtr& b, int level, int depth, double tau,
+                 std::uint64_t I, std::uint64_t K, std::uint64_t J, std::int64_t& count,
+                 std::uint64_t& sum) {
+  if (!a || !b) return;
+  if (a->norm * b->norm < tau) return;
+  if (level == depth) {
+    ++count;
+    sum += digest_mix((I << 42) | (K << 21) | J);
+    return;
+  }
+  for (int row = 0; row < 2; ++row)
+    for (int col = 0; col < 2; ++col)
+      for (int h = 0; h < 2; ++h)
+        digest_walk(a->child[2 * row + h], b->child[2 * h + col], level + 1, depth, tau,
+                    2 * I + row, 2 * K + h, 2 * J + col, count, sum);
+}
+
+struct WalkTask {
+  NodePtr a, b;
+  std::uint64_t I, K, J;
+};
+
+// the surviving level-`top` triples (the same skip test above them)
+void collect_tasks(const NodePtr& a, const NodePtr& b, int level, int top, double tau,
+                   std::uint64_t I, std::uint64_t K, std::uint64_t J, std::vector<WalkTask>& out) {
+  if (!a || !b) return;
+  if (a->norm * b->norm < tau) return;
+  if (level == top) {
+    out.push_back({a, b, I, K, J});
+    return;
+  }
+  for (int row = 0; row < 2; ++row)
+    for (int col = 0; col < 2; ++col)
+      for (int h = 0; h < 2; ++h)
+        collect_tasks(a->child[2 * row + h], b->child[2 * h + col], level + 1, top, tau,
+                      2 * I + row, 2 * K + h, 2 * J + col, out);
+}
+
 }  // namespace
 
 extern "C" {
+
+// Survivor-set digest of spamm_multiply(a, b, tau): the reference trees' own
+// norms and skip rule, walked on `threads` host threads (the sum is order-free)
+void ref_survivor_digest(const void* a, const void* b, double tau, int threads,
+                         std::int64_t* count, std::uint64_t* digest) {
+  const auto* ra = static_cast<const RefTree*>(a);
+  const auto* rb = static_cast<const RefTree*>(b);
+  const int depth = ra->depth;
+  const int top = std::min(depth, 4);
+  std::vector<WalkTask> tasks;
+  collect_tasks(ra->m.root(), rb->m.root(), 0, top, tau, 0, 0, 0, tasks);
+  std::atomic<std::size_t> next{0};
+  std::vector<std::int64_t> counts(static_cast<std::size_t>(std::max(threads, 1)), 0);
+  std::vector<std::uint64_t> sums(counts.size(), 0);
+  std::vector<std::thread> pool;
+  for (std::size_t t = 0; t < counts.size(); ++t)
+    pool.emplace_back([&, t] {
+      for (std::size_t i = next++; i < tasks.size(); i = next++)
+        digest_walk(tasks[i].a, tasks[i].b, top, depth, tau, tasks[i].I, tasks[i].K, tasks[i].J,
+                    counts[t], sums[t]);
+    });
+  for (auto& th : pool) th.join();
+  *count = 0;
+  *digest = 0;
+  for (std::size_t t = 0; t < counts.size(); ++t) {
+    *count += counts[t];
+    *digest += sums[t];
+  }
+}
 
 void* ref_build(int dimension, int leaf, std::int64_t n, const std::int32_t* rows,
                 const std::int32_t* cols, const double* payload) {

@@ -179,6 +179,8 @@ _SIGNATURES = {
     "spg_matrix_from_diagonal": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.POINTER(_vp)]),
     "spg_matrix_rows": (C.c_int, [_vp, _dp, _dp]),
     "spg_matrix_gershgorin": (C.c_int, [_vp, _dp, _dp]),
+    "spg_survivor_digest": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, _i64p,
+                                      C.POINTER(C.c_uint64)]),
     "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
                                              _dp, C.POINTER(C.c_uint8), C.POINTER(_vp)]),
     "spg_matrix_gather_rows": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int64, _vp]),
@@ -514,6 +516,15 @@ def spamm_with_error_control_to_host(ctx: Context, a: Matrix, b: Matrix, delta: 
         _ptr(norms, C.c_double), C.byref(count), _ptr(bounds, C.c_double), C.byref(st)))
     n = count.value
     return (rows[:n], cols[:n], pay[:n], norms[:n]), st.as_dict(), bounds
+
+
+def survivor_digest(ctx: Context, a: Matrix, b: Matrix, tau: float, level: int = 0,
+                    shard: int = 0):
+    """(count, digest) of the survivor set (spg_survivor_digest)."""
+    count, dig = C.c_int64(0), C.c_uint64(0)
+    _check(lib().spg_survivor_digest(ctx.handle, a.handle, b.handle, tau, level, shard,
+                                     C.byref(count), C.byref(dig)))
+    return count.value, dig.value
 
 
 def survivors(ctx: Context, a: Matrix, b: Matrix, tau: float) -> np.ndarray:

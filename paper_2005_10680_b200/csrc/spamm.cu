@@ -1402,6 +1402,58 @@ int spg_spamm_with_error_control_to_host(spg_context* ctx, const spg_matrix* a,
   SPG_API_END
 }
 
+namespace spg {
+namespace {
+__device__ __forceinline__ uint64_t digest_mix(uint64_t z) {  // SplitMix64 finaliser
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// sum over the task list of mix64(i << 42 | k << 21 | j), mod 2^64 (order-free)
+__global__ void survivor_digest_kernel(const uint64_t* __restrict__ keys, int64_t n, int kbits,
+                                       unsigned long long* __restrict__ sum) {
+  unsigned long long local = 0;
+  const uint64_t kmask = (uint64_t(1) << kbits) - 1;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = keys[t], ij = key >> kbits;
+    const uint64_t i = morton_row(ij), j = morton_col(ij), k = key & kmask;
+    local += digest_mix((i << 42) | (k << 21) | j);
+  }
+  for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+  if ((threadIdx.x & 31) == 0) atomicAdd(sum, local);
+}
+}  // namespace
+}  // namespace spg
+
+int spg_survivor_digest(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                        int32_t level, int32_t shard, int64_t* count, uint64_t* digest) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b || !count || !digest) fail(SPG_EINVAL, "null argument");
+  if (a->dimension != b->dimension || a->leaf != b->leaf)
+    fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
+  if (tau < 0.0) fail(SPG_EINVAL, "spamm: tau must be nonnegative");
+  if (level < 0 || level > a->depth || shard < 0 || shard >= (1 << level))
+    fail(SPG_EINVAL, "shard outside the tree");
+  CtxGuard g(ctx);
+  TaskList tl = build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, Shard{level, shard});
+  DevBuf<unsigned long long> sum(1, ctx);
+  SPG_CUDA(cudaMemsetAsync(sum.get(), 0, sizeof(unsigned long long), ctx->stream));
+  if (tl.n_surv) {
+    survivor_digest_kernel<<<grid_for(tl.n_surv, 256, int64_t(ctx->sm_count) * 8), 256, 0,
+                             ctx->stream>>>(tl.keys.get(), tl.n_surv, tl.kbits, sum.get());
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  unsigned long long h = 0;
+  SPG_CUDA(cudaMemcpyAsync(&h, sum.get(), sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *count = tl.n_surv;
+  *digest = h;
+  SPG_API_END
+}
+
 int spg_parity_audit(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                      int32_t ulps, int64_t* near_ties, int64_t* candidates) {
   SPG_API_BEGIN
