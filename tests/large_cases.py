@@ -31,6 +31,8 @@ ELL, DENS, SITE, SEED_A, SEED_B, DROP = 4.0, 0.1, 2005, 10680, 10681, 1e-10
 
 # name -> (N, L, n_taus, tau_lo, deltas, sample delta index or None)
 CASES = {
+    # a small case of the same form (pipeline check; depth 8)
+    "mini": (16384, 64, 64, 1e-14, [1e-6], 0),
     # config 4 as BASELINE.json states it (64 tau over the config-1 range):
     # no tau meets delta = 1e-6 -> tau = 0, the exact product
     "cfg4": (262144, 64, 64, 1e-12, [1e-6], None),
