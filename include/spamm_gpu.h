@@ -27,6 +27,7 @@
 #ifndef SPAMM_GPU_H
 #define SPAMM_GPU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -390,6 +391,49 @@ int spg_matrix_from_leaf_norms(spg_context* ctx, int32_t dimension, int32_t leaf
  * caller knows the count from the leaf table).  `stream` as above. */
 int spg_matrix_gather_rows(const spg_matrix* m, int32_t row_begin, int32_t row_end,
                            double* d_out, int64_t capacity, void* stream);
+
+/* ---- multi-GPU inside the library: communicator + sharded products
+ * (replaces the reference's fork-join over host threads,
+ * execution.cpp:11-23, multiply.cpp:79-84, error_control.cpp:59-66) ---------
+ * One process per GPU; 2^s ranks shard the output block rows: rank r owns
+ * rows [r nb/2^s, (r+1) nb/2^s).  The sweep runs below level s per rank, the
+ * level-s partial vectors are all-gathered and every rank finishes the top s
+ * levels in reference order: bounds and tau are bit-identical to one GPU on
+ * every rank, and so are the rank's rows of C~ (per-block k order unchanged).
+ * Transports: NCCL (loaded with dlopen; SPG_NCCL_LIB overrides the library
+ * name; collectives on the context's stream, over NVLink / NVSwitch) or a
+ * host all-gather callback (the caller's own collective: gloo, MPI, tests). */
+typedef struct spg_comm spg_comm;
+#define SPG_COMM_ID_BYTES 128
+/* All-gather `bytes` from every rank into recv (nranks * bytes, rank order);
+ * return 0 on success. */
+typedef int (*spg_host_allgather_fn)(void* user, const void* send, size_t bytes, void* recv);
+/* ncclGetUniqueId: rank 0 creates it and hands the 128 bytes to the others. */
+int spg_comm_unique_id(void* id_out);
+int spg_comm_create_nccl(spg_context* ctx, int32_t nranks, int32_t rank, const void* id,
+                         spg_comm** out);
+int spg_comm_create_host(spg_context* ctx, int32_t nranks, int32_t rank,
+                         spg_host_allgather_fn fn, void* user, spg_comm** out);
+int spg_comm_info(const spg_comm* comm, int32_t* nranks, int32_t* rank, int32_t* uses_nccl);
+int spg_comm_destroy(spg_comm* comm);
+/* cse (error_control.cpp:160-166) of the whole product, sharded: bounds on
+ * every rank. */
+int spg_cse_sharded(spg_comm* comm, const spg_matrix* a, const spg_matrix* b, const double* taus,
+                    int32_t n_taus, double* bounds);
+/* spamm_multiply (skip_test = 1) / multiply_exact (skip_test = 0), sharded:
+ * the rank's rows of C, or with gather = 1 the whole C on every rank
+ * (all-gather of the rows' leaves). */
+int spg_spamm_sharded(spg_comm* comm, const spg_matrix* a, const spg_matrix* b, double tau,
+                      int32_t skip_test, int32_t gather, spg_matrix** c, spg_spamm_stats* stats);
+/* spamm_with_error_control (error_control.cpp:203-220), sharded as above;
+ * stats->spamm counts this rank's rows; bounds (may be NULL) the whole
+ * problem's. */
+int spg_spamm_with_error_control_sharded(spg_comm* comm, const spg_matrix* a,
+                                         const spg_matrix* b, double delta, const double* taus,
+                                         int32_t n_taus, int32_t gather, spg_matrix** c,
+                                         double* bounds, spg_controlled_stats* stats);
+/* Every rank's row shard (disjoint block rows) -> the whole matrix on every rank. */
+int spg_matrix_gather_shards(spg_comm* comm, const spg_matrix* shard, spg_matrix** out);
 
 #ifdef __cplusplus
 }

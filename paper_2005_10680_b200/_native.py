@@ -179,6 +179,19 @@ _SIGNATURES = {
     "spg_matrix_from_diagonal": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.POINTER(_vp)]),
     "spg_matrix_rows": (C.c_int, [_vp, _dp, _dp]),
     "spg_matrix_gershgorin": (C.c_int, [_vp, _dp, _dp]),
+    "spg_comm_unique_id": (C.c_int, [_vp]),
+    "spg_comm_create_nccl": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
+    "spg_comm_create_host": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, C.POINTER(_vp)]),
+    "spg_comm_info": (C.c_int, [_vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                C.POINTER(C.c_int32)]),
+    "spg_comm_destroy": (C.c_int, [_vp]),
+    "spg_cse_sharded": (C.c_int, [_vp, _vp, _vp, _dp, C.c_int32, _dp]),
+    "spg_spamm_sharded": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32,
+                                    C.POINTER(_vp), _vp]),
+    "spg_spamm_with_error_control_sharded": (C.c_int, [_vp, _vp, _vp, C.c_double, _dp,
+                                                       C.c_int32, C.c_int32, C.POINTER(_vp),
+                                                       _dp, _vp]),
+    "spg_matrix_gather_shards": (C.c_int, [_vp, _vp, C.POINTER(_vp)]),
     "spg_survivor_digest": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32, _i64p,
                                       C.POINTER(C.c_uint64)]),
     "spg_matrix_from_leaf_norms": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int64, _i32p, _i32p,
@@ -493,6 +506,107 @@ def spamm_with_error_control(ctx: Context, a: Matrix, b: Matrix, delta: float, t
                                               _ptr(taus, C.c_double), taus.size, C.byref(h),
                                               _ptr(bounds, C.c_double), C.byref(st)))
     return Matrix(ctx, h), st.as_dict(), bounds
+
+
+# ---------------------------------------------------------------- communicator
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class Comm:
+    """spg_comm: ranks of one job, one GPU each.  nccl(ctx, nranks, rank, id)
+    or host(ctx, nranks, rank, allgather) where allgather(bytes) -> list of
+    per-rank bytes (the caller's own collective, e.g. gloo)."""
+
+    def __init__(self, ctx: Context, handle, keep=None):
+        self.ctx, self._h, self._keep = ctx, handle, keep
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().spg_comm_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, ctx: Context, nranks: int, rank: int, uid: bytes):
+        h = _vp()
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _check(lib().spg_comm_create_nccl(ctx.handle, nranks, rank, buf, C.byref(h)))
+        return cls(ctx, h)
+
+    @classmethod
+    def host(cls, ctx: Context, nranks: int, rank: int, allgather):
+        def cb(_user, send, nbytes, recv):
+            try:
+                parts = allgather(C.string_at(send, nbytes) if nbytes else b"")
+                blob = b"".join(parts)
+                if len(blob) != nbytes * nranks:
+                    return 1
+                if nbytes:
+                    C.memmove(recv, blob, len(blob))
+                return 0
+            except Exception:  # noqa: BLE001 -- reported as SPG_ENCCL by the library
+                return 1
+        fn = HOST_ALLGATHER(cb)
+        h = _vp()
+        _check(lib().spg_comm_create_host(ctx.handle, nranks, rank, C.cast(fn, _vp), None,
+                                          C.byref(h)))
+        return cls(ctx, h, keep=fn)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        n, r, u = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().spg_comm_info(self._h, C.byref(n), C.byref(r), C.byref(u)))
+        return n.value, r.value, bool(u.value)
+
+    def close(self):
+        if self._h:
+            _check(lib().spg_comm_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+def cse_sharded(comm: Comm, a: Matrix, b: Matrix, taus) -> np.ndarray:
+    taus = np.ascontiguousarray(taus, np.float64)
+    out = np.empty(taus.size)
+    _check(lib().spg_cse_sharded(comm.handle, a.handle, b.handle, _ptr(taus, C.c_double),
+                                 taus.size, _ptr(out, C.c_double)))
+    return out
+
+
+def spamm_sharded(comm: Comm, a: Matrix, b: Matrix, tau: float, skip_test: bool = True,
+                  gather: bool = False):
+    h = _vp()
+    st = SpammStats()
+    _check(lib().spg_spamm_sharded(comm.handle, a.handle, b.handle, tau, int(skip_test),
+                                   int(gather), C.byref(h), C.byref(st)))
+    return Matrix(comm.ctx, h), st.as_dict()
+
+
+def spamm_with_error_control_sharded(comm: Comm, a: Matrix, b: Matrix, delta: float, taus,
+                                     gather: bool = False):
+    taus = np.ascontiguousarray(taus, np.float64)
+    bounds = np.empty(taus.size, np.float64)
+    h = _vp()
+    st = ControlledStats()
+    _check(lib().spg_spamm_with_error_control_sharded(comm.handle, a.handle, b.handle, delta,
+                                                      _ptr(taus, C.c_double), taus.size,
+                                                      int(gather), C.byref(h),
+                                                      _ptr(bounds, C.c_double), C.byref(st)))
+    return Matrix(comm.ctx, h), st.as_dict(), bounds
+
+
+def gather_shards(comm: Comm, shard: Matrix) -> Matrix:
+    h = _vp()
+    _check(lib().spg_matrix_gather_shards(comm.handle, shard.handle, C.byref(h)))
+    return Matrix(comm.ctx, h)
 
 
 def spamm_with_error_control_to_host(ctx: Context, a: Matrix, b: Matrix, delta: float, taus,

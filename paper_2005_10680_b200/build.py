@@ -30,7 +30,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-Wno-deprecated-declarations", "-Xcompiler", "-ffp-contract=off",
     f"-I{INCLUDE}", f"-I{CSRC}",
 ]
-CU_SOURCES = ["norms.cu", "matrix.cu", "cse.cu", "spamm.cu", "synth.cu", "truncate.cu", "algebra.cu", "purify.cu", "bstream.cu"]
+CU_SOURCES = ["norms.cu", "matrix.cu", "cse.cu", "spamm.cu", "synth.cu", "truncate.cu", "algebra.cu", "purify.cu", "bstream.cu", "comm.cu"]
 HEADERS = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)]
 
 CXX = os.environ.get("CXX", "g++")

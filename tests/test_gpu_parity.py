@@ -86,6 +86,30 @@ def test_cfg1_on_gpu_matches_reference_golden(ctx):
     assert realized <= st["bound"] * (1 + 1e-9) + 1e-10 * np.linalg.norm(d) ** 2 * 1e-6
 
 
+def test_cfg1_c_elementwise_vs_reference(ctx, ref):
+    """Config 1's C~ block by block against the reference's own
+    spamm_multiply (oracle/_ref, all host threads) at the reference's tau*:
+    identical block structure, every block within 1e-12 relative Frobenius,
+    every C~ leaf norm within the same tolerance."""
+    import os
+    from paper_2005_10680_b200 import _native as nat
+    meta = json.loads((GOLDEN / "cfg1.json").read_text())
+    rows, cols, pay = nat.synth_chain_host(meta["n"], meta["leaf"], meta["ell"], meta["seed"],
+                                           meta["drop"])
+    A = nat.upload(ctx, meta["n"], meta["leaf"], rows, cols, pay)
+    g = load_golden("cfg1")
+    C, st, _ = nat.spamm_with_error_control(ctx, A, A, meta["delta"], g["taus"])
+    ref.set_threads(os.cpu_count() or 1)
+    T = ref.build(meta["n"], meta["leaf"], rows, cols, pay)
+    rr, rc, rp, rn = ref.spamm(T, T, st["tau"]).leaves()
+    r, c, p, nrm = C.download()
+    assert np.array_equal(r, rr) and np.array_equal(c, rc)
+    assert rel_fro(p, rp) < REL_TOL
+    per_block = np.linalg.norm(p - rp, axis=1) / np.maximum(np.linalg.norm(rp, axis=1), 1e-300)
+    assert per_block.max() < REL_TOL, per_block.max()
+    assert np.all(np.abs(nrm - rn) <= REL_TOL * rn)
+
+
 def _random_case(rng, n, L, fill, decay):
     d = np.where(rng.uniform(size=(n, n)) < fill, rng.uniform(-1, 1, (n, n)), 0.0)
     if decay:
