@@ -36,7 +36,7 @@ HEADERS = list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h")) + [Path(__file__)
 CXX = os.environ.get("CXX", "g++")
 DROPIN_SOURCES = ["dropin/quadtree.cpp", "dropin/multiply.cpp", "dropin/error_control.cpp",
                   "dropin/matrix_market.cpp", "dropin/experiment.cpp",
-                  "dropin/purification.cpp", "dropin/runtime.cpp"]
+                  "dropin/purification.cpp", "dropin/runtime.cpp", "dropin/distributed.cpp"]
 
 
 def _stale(target: Path, deps) -> bool:

@@ -38,8 +38,12 @@ ErrorBoundVector cse(const QuadTreeMatrix& a, const QuadTreeMatrix& b, const Tol
   if (a.dimension() != b.dimension() || a.leaf_size() != b.leaf_size())
     throw std::invalid_argument("cse: dimension or leaf size mismatch");
   ErrorBoundVector out{std::vector<double>(grid.size())};
-  b200::check(spg_cse(b200::context(), a.device(), b.device(), grid.taus().data(),
-                      static_cast<int32_t>(grid.size()), out.bounds.data()));
+  if (spg_comm* comm = b200::communicator())
+    b200::check(spg_cse_sharded(comm, a.device(), b.device(), grid.taus().data(),
+                                static_cast<int32_t>(grid.size()), out.bounds.data()));
+  else
+    b200::check(spg_cse(b200::context(), a.device(), b.device(), grid.taus().data(),
+                        static_cast<int32_t>(grid.size()), out.bounds.data()));
   return out;
 }
 
@@ -77,9 +81,14 @@ ControlledProduct spamm_with_error_control(const QuadTreeMatrix& a, const QuadTr
     throw std::invalid_argument("cse: dimension or leaf size mismatch");
   spg_matrix* c = nullptr;
   spg_controlled_stats st{};
-  b200::check(spg_spamm_with_error_control(b200::context(), a.device(), b.device(), delta,
-                                           grid.taus().data(), static_cast<int32_t>(grid.size()),
-                                           &c, nullptr, &st));
+  if (spg_comm* comm = b200::communicator())  // row shards, C gathered on every rank
+    b200::check(spg_spamm_with_error_control_sharded(
+        comm, a.device(), b.device(), delta, grid.taus().data(),
+        static_cast<int32_t>(grid.size()), 1, &c, nullptr, &st));
+  else
+    b200::check(spg_spamm_with_error_control(b200::context(), a.device(), b.device(), delta,
+                                             grid.taus().data(),
+                                             static_cast<int32_t>(grid.size()), &c, nullptr, &st));
   ControlledProduct out;
   out.matrix = adopt_device(c);
   out.chosen_tau = SpammTolerance{st.tau};

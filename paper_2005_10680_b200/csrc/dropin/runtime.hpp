@@ -13,6 +13,9 @@ namespace spamm::b200 {
 /// Process-wide context on device $SPAMM_B200_DEVICE (default 0).
 spg_context* context();
 
+/// The multi-GPU communicator (spamm::distributed), or null: single GPU.
+spg_comm* communicator();
+
 /// Map a C-ABI status onto the reference's exception types
 /// (std::invalid_argument / std::out_of_range, include/spamm_gpu.h).
 void check(int rc);
