@@ -85,6 +85,13 @@ int spg_context_stream(spg_context* ctx, void** stream);
 int spg_context_synchronize(spg_context* ctx);
 /* Kernel launches issued by this context so far (evidence counter). */
 int spg_context_launch_count(spg_context* ctx, int64_t* launches);
+/* Products larger than the device's memory (the reference's spamm_multiply
+ * has no size cap, multiply.cpp:109-116): when a product's task list (at
+ * most ~40 B per candidate leaf product) would exceed `bytes` -- 0 (default):
+ * half of the free HBM plus the context's cached pool -- the product is run
+ * in 2^c row chunks, one task list at a time, into one C; bitwise the same C
+ * (same products, same per-block k order). */
+int spg_context_set_task_budget(spg_context* ctx, int64_t bytes);
 
 /* ---- matrices (quadtree.hpp / quadtree.cpp) ------------------------------ */
 /* Replaces QuadTreeMatrix::from_coordinates at leaf granularity
@@ -358,6 +365,21 @@ int spg_plan_accumulate(spg_plan* plan, int32_t row_begin, int32_t row_end,
                         const double* d_panel, void* stream);
 int spg_plan_finish(spg_plan* plan, spg_matrix** c, spg_spamm_stats* stats);
 void spg_plan_free(spg_plan* plan);
+/* The whole panel loop in one call, with the row chunking of
+ * spg_context_set_task_budget (each chunk receives every panel again): B's
+ * panels of `panel_rows` block rows (never crossing a multiple of
+ * `owner_rows`, 0 = no owners) are requested from fetch(user, row_begin,
+ * row_end, d_dst, count, stream), which fills d_dst with the `count` leaves of
+ * those rows in (row, col) order on `stream` (asynchronously is fine: the
+ * GEMM waits for the stream; the buffer is not refilled before its GEMM is
+ * done).  Two panels are in flight.  The context is unlocked while fetch
+ * runs.  Returns the shard's rows of C~ -- bitwise the resident product's. */
+typedef int (*spg_panel_fetch_fn)(void* user, int32_t row_begin, int32_t row_end, double* d_dst,
+                                  int64_t count, void* stream);
+int spg_spamm_panels(spg_context* ctx, const spg_matrix* a, const spg_matrix* a_norms,
+                     const spg_matrix* b_norms, double tau, int32_t level, int32_t shard,
+                     int32_t panel_rows, int32_t owner_rows, spg_panel_fetch_fn fetch,
+                     void* user, spg_matrix** c, spg_spamm_stats* stats);
 /* All of the plan's products in ONE GEMM launch, B leaf t read in place
  * from owner_base[slot_owner[t]] + slot_local[t] * L*L: the owners' leaf
  * payloads, local or another GPU's memory opened with spg_ipc_open (NVLink

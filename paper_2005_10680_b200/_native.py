@@ -179,6 +179,9 @@ _SIGNATURES = {
     "spg_matrix_from_diagonal": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, C.POINTER(_vp)]),
     "spg_matrix_rows": (C.c_int, [_vp, _dp, _dp]),
     "spg_matrix_gershgorin": (C.c_int, [_vp, _dp, _dp]),
+    "spg_context_set_task_budget": (C.c_int, [_vp, C.c_int64]),
+    "spg_spamm_panels": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32,
+                                   C.c_int32, C.c_int32, _vp, _vp, C.POINTER(_vp), _vp]),
     "spg_comm_unique_id": (C.c_int, [_vp]),
     "spg_comm_create_nccl": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.POINTER(_vp)]),
     "spg_comm_create_host": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, _vp, C.POINTER(_vp)]),
@@ -506,6 +509,49 @@ def spamm_with_error_control(ctx: Context, a: Matrix, b: Matrix, delta: float, t
                                               _ptr(taus, C.c_double), taus.size, C.byref(h),
                                               _ptr(bounds, C.c_double), C.byref(st)))
     return Matrix(ctx, h), st.as_dict(), bounds
+
+
+# ---------------------------------------------------------------- beyond one device's memory
+PANEL_FETCH = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
+                          C.c_void_p)
+
+
+def set_task_budget(ctx: Context, nbytes: int):
+    """Row-chunk products whose task list would exceed nbytes (0: auto)."""
+    _check(lib().spg_context_set_task_budget(ctx.handle, int(nbytes)))
+
+
+class DevicePtr:
+    """A float64 view of device memory for torch.as_tensor (no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def spamm_panels(ctx: Context, a: Matrix, b_norms: Matrix, tau: float, fetch, level: int = 0,
+                 shard: int = 0, panel_rows: int = 32, owner_rows: int = 0,
+                 a_norms: Matrix | None = None):
+    """spg_spamm_panels: the shard's rows of C~ with B's panels requested from
+    fetch(r0, r1, d_dst_ptr, count, stream_ptr) (fills count leaves of rows
+    [r0, r1) in (row, col) order on the stream); row-chunked in C when the
+    task list would not fit."""
+    def cb(_user, r0, r1, dst, count, stream):
+        try:
+            fetch(int(r0), int(r1), int(dst or 0), int(count), int(stream or 0))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported as SPG_EINVAL by the library
+            import traceback
+            traceback.print_exc()
+            return 1
+    fn = PANEL_FETCH(cb)
+    h = _vp()
+    st = SpammStats()
+    _check(lib().spg_spamm_panels(ctx.handle, a.handle, a_norms.handle if a_norms else None,
+                                  b_norms.handle, tau, level, shard, panel_rows, owner_rows,
+                                  C.cast(fn, _vp), None, C.byref(h), C.byref(st)))
+    return Matrix(ctx, h), st.as_dict()
 
 
 # ---------------------------------------------------------------- communicator (SURVEY 8e)

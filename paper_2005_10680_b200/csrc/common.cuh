@@ -83,6 +83,7 @@ struct spg_context {
   std::mutex mu;
   int64_t launches = 0;   // own kernels launched (evidence counter)
   int64_t lib_calls = 0;  // CUB primitives invoked
+  int64_t task_budget = 0;  // task-list bytes per product before row chunking (0: free HBM)
   spg::DevicePool pool;
 };
 
@@ -222,6 +223,8 @@ spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32
                                       int64_t n_blocks, uint64_t* d_keys_owned,
                                       double* d_payload_owned);
 void matrix_destroy(spg_matrix* m);
+// one matrix from row chunks (disjoint block rows) -- leaves copied, norms recomputed (K1)
+spg_matrix* concat_row_chunks(spg_context* ctx, const std::vector<spg_matrix*>& parts);
 // New matrix over x's payload (shared) keeping the slots with keep[slot] != 0;
 // slot_norms[slot] = cached leaf norm (K1 result) for kept slots.
 spg_matrix* matrix_keep_slots(spg_context* ctx, const spg_matrix* x, const double* slot_norms,

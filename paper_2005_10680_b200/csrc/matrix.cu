@@ -420,6 +420,45 @@ spg_matrix* matrix_from_morton_blocks(spg_context* ctx, int32_t dimension, int32
   return m.release();
 }
 
+namespace {
+__global__ void pack_chunk(const uint64_t* __restrict__ keys, const int32_t* __restrict__ slots,
+                           int64_t n, const double* __restrict__ payload, int64_t LL,
+                           uint64_t* __restrict__ out_keys, double* __restrict__ out) {
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    if (threadIdx.x == 0) out_keys[t] = keys[t];
+    const double* src = payload + static_cast<int64_t>(slots[t]) * LL;
+    for (int64_t e = threadIdx.x; e < LL; e += blockDim.x) out[t * LL + e] = src[e];
+  }
+}
+}  // namespace
+
+spg_matrix* concat_row_chunks(spg_context* ctx, const std::vector<spg_matrix*>& parts) {
+  if (parts.empty()) fail(SPG_EINTERNAL, "concat: no parts");
+  const spg_matrix* f = parts[0];
+  const int64_t LL = static_cast<int64_t>(f->leaf) * f->leaf;
+  int64_t total = 0;
+  for (const spg_matrix* m : parts) total += m->nnzb;
+  double* pay = dev_alloc<double>(std::max<int64_t>(total * LL, 1), ctx);
+  uint64_t* keys = nullptr;
+  try {
+    keys = dev_alloc<uint64_t>(std::max<int64_t>(total, 1), ctx);
+    int64_t off = 0;
+    for (const spg_matrix* m : parts) {
+      if (m->nnzb) {
+        pack_chunk<<<grid_for(m->nnzb, 1, 1 << 20), 256, 0, ctx->stream>>>(
+            m->keys, m->slots, m->nnzb, m->payload, LL, keys + off, pay + off * LL);
+        SPG_CHECK_LAUNCH(ctx);
+      }
+      off += m->nnzb;
+    }
+  } catch (...) {
+    dev_free(pay, ctx);
+    if (keys) dev_free(keys, ctx);
+    throw;
+  }
+  return matrix_from_morton_blocks(ctx, f->dimension, f->leaf, total, keys, pay);
+}
+
 }  // namespace spg
 
 using namespace spg;
@@ -484,6 +523,14 @@ int spg_context_synchronize(spg_context* ctx) {
   if (!ctx) fail(SPG_EINVAL, "null context");
   CtxGuard g(ctx);
   SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  SPG_API_END
+}
+
+int spg_context_set_task_budget(spg_context* ctx, int64_t bytes) {
+  SPG_API_BEGIN
+  if (!ctx) fail(SPG_EINVAL, "null context");
+  if (bytes < 0) fail(SPG_EINVAL, "task budget must be >= 0");
+  ctx->task_budget = bytes;
   SPG_API_END
 }
 

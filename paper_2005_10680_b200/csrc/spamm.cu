@@ -882,6 +882,117 @@ void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_mat
 
 }  // namespace
 
+// Row chunks of a product whose task list would not fit (include/spamm_gpu.h
+// spg_context_set_task_budget): 2^c sub-shards of `sh`, one task list at a
+// time.  ~40 B per candidate bounds the build's peak (triples, masks, keys
+// and their sorted copy, pairs).
+int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard sh,
+               int max_bits) {
+  if (max_bits <= 0) return 0;
+  int64_t budget = ctx->task_budget;
+  if (budget <= 0) {
+    size_t fr = 0, tot = 0;
+    SPG_CUDA(cudaMemGetInfo(&fr, &tot));
+    size_t cached = 0;
+    for (const auto& kv : ctx->pool.free_blocks) cached += kv.first;
+    budget = static_cast<int64_t>((fr + cached) / 2);
+  }
+  const double need = 40.0 * static_cast<double>(count_candidates(ctx, a, b, sh));
+  int c = 0;
+  while (c < max_bits && need / static_cast<double>(int64_t(1) << c) > static_cast<double>(budget))
+    ++c;
+  return c;
+}
+
+void gemm_plan(spg_context* ctx, int depth, int L, const Plan& plan, bool super32,
+               const double* A, const double* B, const double* const* btab, double* C) {
+  if (super32) {
+    PhaseTrace tr(ctx, "gemm(super32)");
+    run_super32(ctx, depth, plan, A, btab, C);
+  } else if (L == 128 && sub128_enabled()) {
+    PhaseTrace tr(ctx, "gemm(sub128)");
+    run_sub128(ctx, plan, A, btab, C);
+  } else {
+    DevBuf<int32_t> order = make_block_order(ctx, plan.out_keys.get(), plan.n_out, plan.n_out);
+    PhaseTrace tr(ctx, "gemm");
+    run_gemm(ctx, L, A, B, plan.pairs.get(), plan.out_offset.get(), plan.n_out, C, nullptr,
+             nullptr, 0, btab, order.get());
+  }
+}
+
+// The product in 2^c row chunks: pass 1 sizes every chunk's output (its task
+// list, then freed), pass 2 rebuilds each chunk's task list and runs its GEMM
+// into its rows' place in one C payload.  Per block the same pairs in the
+// same k order: C is bitwise the unchunked product.
+spg_matrix* spamm_device_chunked(spg_context* ctx, const spg_matrix* a, const spg_matrix* b,
+                                 double tau, bool skip_test, spg_spamm_stats* stats, Shard sh,
+                                 int c, bool super32) {
+  const int L = a->leaf;
+  const int64_t LL = static_cast<int64_t>(L) * L;
+  const int nch = 1 << c;
+  auto sub = [&](int q) { return Shard{sh.level + c, (sh.index << c) + q}; };
+  std::vector<int64_t> n_out(static_cast<size_t>(nch));
+  int64_t total_out = 0;
+  for (int q = 0; q < nch; ++q) {
+    const Plan pl = plan_product(ctx, a, b, tau, skip_test, sub(q), false);
+    n_out[q] = pl.n_out;
+    total_out += pl.n_out;
+  }
+  double* c_payload = dev_alloc<double>(std::max<int64_t>(total_out * LL, 1), ctx);
+  uint64_t* keys = nullptr;
+  try {
+    keys = dev_alloc<uint64_t>(std::max<int64_t>(total_out, 1), ctx);
+  } catch (...) {
+    dev_free(c_payload, ctx);
+    throw;
+  }
+  const double* const* btab = leaf_table(ctx, b);
+  float ms_task = 0.0f, ms_gemm = 0.0f;
+  int64_t n_surv = 0, off = 0;
+  try {
+    for (int q = 0; q < nch; ++q) {
+      SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
+      Plan pl = plan_product(ctx, a, b, tau, skip_test, sub(q), super32);
+      SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
+      if (pl.n_out != n_out[q]) fail(SPG_EINTERNAL, "chunked product: chunk size changed");
+      if (pl.n_out) {
+        gemm_plan(ctx, a->depth, L, pl, super32, a->payload, b->payload, btab,
+                  c_payload + off * LL);
+        SPG_CUDA(cudaMemcpyAsync(keys + off, pl.out_keys.get(), pl.n_out * sizeof(uint64_t),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+      SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+      SPG_CUDA(cudaEventSynchronize(ctx->ev[4]));
+      float t1 = 0.0f, t2 = 0.0f;
+      SPG_CUDA(cudaEventElapsedTime(&t1, ctx->ev[2], ctx->ev[3]));
+      SPG_CUDA(cudaEventElapsedTime(&t2, ctx->ev[3], ctx->ev[4]));
+      ms_task += t1;
+      ms_gemm += t2;
+      n_surv += pl.n_surv;
+      off += pl.n_out;
+    }
+  } catch (...) {
+    dev_free(keys, ctx);
+    dev_free(c_payload, ctx);
+    throw;
+  }
+  SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
+  // chunk keys are not globally in Morton order: the matrix scatters them
+  spg_matrix* out = matrix_from_morton_blocks(ctx, a->dimension, L, total_out, keys, c_payload);
+  SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
+  SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
+  if (stats) {
+    stats->survivors = n_surv;
+    stats->output_blocks = total_out;
+    stats->flops = 2.0 * static_cast<double>(L) * L * L * static_cast<double>(n_surv);
+    stats->ms_tasklist = ms_task;
+    stats->ms_gemm = ms_gemm;
+    SPG_CUDA(cudaEventElapsedTime(&stats->ms_finalize, ctx->ev[4], ctx->ev[5]));
+    stats->candidates = count_candidates(ctx, a, b, sh);
+  }
+  return out;
+}
+
 spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                          bool skip_test, spg_spamm_stats* stats, Shard shard, HostOut* host) {
   if (a->dimension != b->dimension || a->leaf != b->leaf)
@@ -894,8 +1005,12 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     fail(SPG_EINVAL, "spamm: shard outside the quadtree");
   const int L = a->leaf;
   const int64_t LL = static_cast<int64_t>(L) * L;
-  SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   const bool super32 = L == 32 && !host && super32_enabled();
+  if (!host) {  // super blocks pair rows 2I, 2I+1: a chunk keeps >= 2 rows for them
+    const int c = chunk_bits(ctx, a, b, shard, a->depth - shard.level - (super32 ? 1 : 0));
+    if (c > 0) return spamm_device_chunked(ctx, a, b, tau, skip_test, stats, shard, c, super32);
+  }
+  SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
   Plan plan = plan_product(ctx, a, b, tau, skip_test, shard, super32);
   const int64_t n_surv = plan.n_surv, n_out = plan.n_out;
   DevBuf<uint64_t>& out_keys = plan.out_keys;
@@ -911,18 +1026,7 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   } else {
     double* c_payload = dev_alloc<double>(std::max<int64_t>(n_out * LL, 1), ctx);
     const double* const* btab = leaf_table(ctx, b);
-    if (super32) {
-      PhaseTrace tr(ctx, "gemm(super32)");
-      run_super32(ctx, a->depth, plan, a->payload, btab, c_payload);
-    } else if (L == 128 && sub128_enabled()) {
-      PhaseTrace tr(ctx, "gemm(sub128)");
-      run_sub128(ctx, plan, a->payload, btab, c_payload);
-    } else {
-      DevBuf<int32_t> order = make_block_order(ctx, out_keys.get(), n_out, n_out);
-      PhaseTrace tr(ctx, "gemm");
-      run_gemm(ctx, L, a->payload, b->payload, pairs.get(), out_offset.get(), n_out, c_payload,
-               nullptr, nullptr, 0, btab, order.get());
-    }
+    gemm_plan(ctx, a->depth, L, plan, super32, a->payload, b->payload, btab, c_payload);
     SPG_CUDA(cudaEventRecord(ctx->ev[4], ctx->stream));
     pairs.reset();
     out_offset.reset();
@@ -1262,6 +1366,104 @@ spg_matrix* spamm_streamed_device(spg_context* ctx, const spg_matrix* a, const s
   return c;
 }
 
+
+// A (shard of a) product whose B arrives in panels from the caller's fetch
+// callback (host memory, NCCL broadcast by the owning GPU, a generator ...),
+// two panels in flight, in 2^c row chunks when the task list would exceed
+// the task budget; each chunk receives every panel again.  The chunks' rows
+// are disjoint, so their C's merge leaf for leaf; bitwise the resident product.
+// The context lock is released while the callback runs (it may call back in).
+spg_matrix* spamm_panels_device(spg_context* ctx, std::unique_lock<std::mutex>& lock,
+                                const spg_matrix* a, const spg_matrix* a_norms,
+                                const spg_matrix* b, double tau, Shard sh, int32_t panel_rows,
+                                int32_t owner_rows, spg_panel_fetch_fn fetch, void* user,
+                                spg_spamm_stats* stats) {
+  if (!b->norms_only || b->row_slot_begin.empty())
+    fail(SPG_EINVAL, "panels: B must be a norm-only matrix (spg_matrix_from_leaf_norms)");
+  if (panel_rows < 1) fail(SPG_EINVAL, "panels: panel_rows must be positive");
+  const int64_t LL = static_cast<int64_t>(a->leaf) * a->leaf;
+  const int32_t nb = (a->dimension + a->leaf - 1) / a->leaf;
+  // panels tile [0, nb) and never cross an owner boundary
+  std::vector<std::pair<int32_t, int32_t>> panels;
+  for (int32_t r = 0; r < nb;) {
+    int32_t r1 = std::min(r + panel_rows, nb);
+    if (owner_rows > 0) r1 = std::min(r1, (r / owner_rows + 1) * owner_rows);
+    panels.push_back({r, r1});
+    r = r1;
+  }
+  const auto& rs = b->row_slot_begin;
+  int64_t cap = 0;
+  for (const auto& pr : panels) cap = std::max(cap, rs[pr.second] - rs[pr.first]);
+  const spg_matrix* an = a_norms ? a_norms : a;
+  const int c = chunk_bits(ctx, an, b, sh, a->depth - sh.level);
+  std::vector<spg_matrix*> parts;
+  struct Parts {
+    std::vector<spg_matrix*>& v;
+    ~Parts() {
+      for (spg_matrix* m : v) matrix_destroy(m);
+    }
+  } guard{parts};
+  spg_spamm_stats total{};
+  DevBuf<double> buf[2] = {DevBuf<double>(std::max<int64_t>(cap * LL, 1), ctx),
+                           DevBuf<double>(std::max<int64_t>(cap * LL, 1), ctx)};
+  cudaStream_t fs[2] = {ctx->copy_stream, ctx->h2d_stream};
+  EventSet ev;  // e[0..1]: buffer i filled; e[2..3]: buffer i free again
+  for (int q = 0; q < (1 << c); ++q) {
+    std::unique_ptr<spg_plan> plan(
+        plan_create(ctx, a, b, tau, Shard{sh.level + c, (sh.index << c) + q}, a_norms));
+    SPG_CUDA(cudaEventRecord(ev.e[2], ctx->stream));
+    SPG_CUDA(cudaEventRecord(ev.e[3], ctx->stream));
+    std::vector<size_t> live;
+    for (size_t p = 0; p < panels.size(); ++p)
+      if (plan->pl.n_out && rs[panels[p].second] > rs[panels[p].first]) live.push_back(p);
+    auto issue = [&](size_t k) {
+      const size_t p = live[k];
+      const int i = static_cast<int>(k & 1);
+      SPG_CUDA(cudaStreamWaitEvent(fs[i], ev.e[2 + i], 0));
+      const int64_t cnt = rs[panels[p].second] - rs[panels[p].first];
+      lock.unlock();
+      const int rc = fetch(user, panels[p].first, panels[p].second, buf[i].get(), cnt, fs[i]);
+      lock.lock();
+      if (rc != 0) fail(SPG_EINVAL, "panels: fetch callback failed for block rows [" +
+                                        std::to_string(panels[p].first) + ", " +
+                                        std::to_string(panels[p].second) + ")");
+      SPG_CUDA(cudaEventRecord(ev.e[i], fs[i]));
+    };
+    if (!live.empty()) issue(0);
+    size_t k = 0;
+    for (size_t p = 0; p < panels.size(); ++p) {
+      if (k < live.size() && live[k] == p) {
+        if (k + 1 < live.size()) issue(k + 1);
+        const int i = static_cast<int>(k & 1);
+        SPG_CUDA(cudaStreamWaitEvent(ctx->stream, ev.e[i], 0));
+        plan_accumulate(plan.get(), panels[p].first, panels[p].second, buf[i].get());
+        SPG_CUDA(cudaEventRecord(ev.e[2 + i], ctx->stream));
+        ++k;
+      } else {
+        plan_accumulate(plan.get(), panels[p].first, panels[p].second, nullptr);
+      }
+    }
+    parts.push_back(plan_finish(plan.get()));
+    const spg_spamm_stats& st = plan->stats;
+    total.candidates += st.candidates;
+    total.survivors += st.survivors;
+    total.output_blocks += st.output_blocks;
+    total.flops += st.flops;
+    total.ms_tasklist += st.ms_tasklist;
+    total.ms_gemm += st.ms_gemm;
+    total.ms_finalize += st.ms_finalize;
+  }
+  SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+  spg_matrix* out = nullptr;
+  if (parts.size() == 1) {
+    out = parts[0];
+    parts.clear();
+  } else {
+    out = concat_row_chunks(ctx, parts);
+  }
+  if (stats) *stats = total;
+  return out;
+}
 
 namespace {
 using Clock = std::chrono::steady_clock;
@@ -1614,6 +1816,24 @@ int spg_plan_run_table(spg_plan* plan, int32_t n_owners, const double* const* ow
   ForeignOrder fo(plan->ctx, stream, plan->ev[0]);
   plan_run_table(plan, tab.data(), n);
   fo.done();
+  SPG_API_END
+}
+
+int spg_spamm_panels(spg_context* ctx, const spg_matrix* a, const spg_matrix* a_norms,
+                     const spg_matrix* b_norms, double tau, int32_t level, int32_t shard,
+                     int32_t panel_rows, int32_t owner_rows, spg_panel_fetch_fn fetch,
+                     void* user, spg_matrix** c, spg_spamm_stats* stats) {
+  SPG_API_BEGIN
+  if (!ctx || !a || !b_norms || !fetch || !c) fail(SPG_EINVAL, "null argument");
+  *c = nullptr;
+  if (a->ctx != ctx || b_norms->ctx != ctx || (a_norms && a_norms->ctx != ctx))
+    fail(SPG_EINVAL, "operands belong to another context");
+  if (level < 0 || level > a->depth || shard < 0 || shard >= (1 << level))
+    fail(SPG_EINVAL, "spamm: shard outside the quadtree");
+  std::unique_lock<std::mutex> lock(ctx->mu);
+  SPG_CUDA(cudaSetDevice(ctx->device));
+  *c = spamm_panels_device(ctx, lock, a, a_norms, b_norms, tau, Shard{level, shard}, panel_rows,
+                           owner_rows, fetch, user, stats);
   SPG_API_END
 }
 

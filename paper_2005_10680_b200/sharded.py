@@ -211,19 +211,41 @@ class DistributedOperands:
             nat.ipc_close(self.ctx, ptr)
         self.opened = []
 
+    def _panels(self, tau, fetch, panel_rows):
+        """Broadcast transport: spg_spamm_panels with fetch(r0, r1, owner, buf,
+        count, stream) adapted from the C callback (device pointer -> torch
+        view, stream pointer -> torch stream).  The library row-chunks the
+        rank's rows when the task list would exceed the context's task budget
+        (spg_context_set_task_budget), each chunk receiving the panels again."""
+        import torch
+        LL = self.L * self.L
+        owner_rows = (1 << nat_depth(self.n, self.L)) >> self.level
+        dev = torch.device("cuda", self.ctx.device)
+        moved = [0]
+
+        def cfetch(r0, r1, dst, count, stream):
+            owner = r0 // owner_rows
+            buf = torch.as_tensor(nat.DevicePtr(dst, max(count, 1) * LL), device=dev)
+            s = torch.cuda.ExternalStream(stream, device=dev)
+            with torch.cuda.stream(s):
+                fetch(r0, r1, owner, buf, count, s)
+            moved[0] += count * LL * 8
+
+        C, st = nat.spamm_panels(self.ctx, self.A, self.B_norms, tau, cfetch, self.level,
+                                 self.rank, panel_rows, owner_rows, a_norms=self.A_norms)
+        return C, st, moved[0]
+
     def controlled_product(self, delta: float, taus, fetch=None, panel_rows: int = 8,
                            row_chunks: int = 1):
         """This rank's rows of spamm_with_error_control(A, B, delta, taus).
 
-        row_chunks = 2^c: the rank's block rows are multiplied in 2^c
-        consecutive sub-shards, one task list at a time, so the task list (16 B
-        per surviving product) never holds more than a 1/2^c share -- config
-        4's ~6e9 products per rank would not fit otherwise.  With the
-        broadcast transport every chunk receives B again (2^c x B per product;
-        config 4 at c = 3: ~3 TB per rank, ~4 s over NVLink against ~130 s of
-        GEMM); the peer transport reads B in place either way.
-        Returns C as one matrix (row_chunks = 1) or the list of chunk
-        matrices in row order."""
+        Broadcast transport: one spg_spamm_panels call; the library splits the
+        rank's rows into task-list chunks by itself when the task list (~40 B
+        per candidate) would not fit (config 4: ~6e9 products per rank), each
+        chunk receiving B's panels again.  Peer transport: row_chunks = 2^c
+        consecutive sub-shards, one task list and one table-addressed GEMM
+        each (B read in place either way); returns the list of chunk matrices
+        in row order when row_chunks > 1."""
         import numpy as np
         if not (delta > 0.0):
             raise ValueError("spamm_with_error_control: delta must be positive")
@@ -241,17 +263,19 @@ class DistributedOperands:
             bounds = nat.cse_finish(level, nat.top_norms(self.A_norms, level),
                                     nat.top_norms(self.B_norms, level), parts)
         tau, k = nat.select_tolerance(bounds, taus, delta)
+        if self.transport == "broadcast":
+            # the whole panel loop in C (spg_spamm_panels): B panels from the
+            # owners through fetch(), row chunks sized by the task budget
+            C, st, moved = self._panels(tau, fetch, panel_rows)
+            return C, {"tau": tau, "tau_index": k,
+                       "bound": float(bounds[k]) if k >= 0 else 0.0, "spamm": st,
+                       "panel_bytes": moved}, bounds
         pieces, stats = [], []
         moved = 0
         for sub in range(1 << c):
             plan = nat.Plan(self.ctx, self.A, self.B_norms, tau, level + c,
                             (self.rank << c) + sub, a_norms=self.A_norms)
-            if self.transport == "peer":
-                plan.run_table(self.bases, self.slot_owner, self.slot_local)
-            else:
-                moved += run_panels(self.ctx, plan,
-                                    panel_schedule(self.n, self.L, level, panel_rows), fetch,
-                                    self.L)
+            plan.run_table(self.bases, self.slot_owner, self.slot_local)
             C, st = plan.finish()
             plan.free()
             pieces.append(C)
@@ -260,12 +284,18 @@ class DistributedOperands:
         for key in ("candidates", "survivors", "output_blocks", "flops", "ms_tasklist", "ms_gemm",
                     "ms_finalize"):
             st[key] = sum(x[key] for x in stats)
-        if self.transport == "peer":
-            mine = self.slot_owner == self.rank
-            moved = int((~mine).sum()) * self.L * self.L * 8  # leaves read remotely (distinct)
+        mine = self.slot_owner == self.rank
+        moved = int((~mine).sum()) * self.L * self.L * 8  # leaves read remotely (distinct)
         return (pieces[0] if c == 0 else pieces), \
             {"tau": tau, "tau_index": k, "bound": float(bounds[k]) if k >= 0 else 0.0,
              "spamm": st, "panel_bytes": moved}, bounds
+
+
+def nat_depth(n: int, leaf: int) -> int:
+    d = 0
+    while (leaf << d) < n:
+        d += 1
+    return d
 
 
 def controlled_product_distributed(ctx, A_local, B_local, delta: float, taus, level: int,

@@ -341,34 +341,64 @@ def test_peer_row_chunks_bitwise(ctx, chunks):
 
 
 @pytest.mark.gpu
-def test_broadcast_row_chunks_bitwise(ctx):
-    """Broadcast transport with the rows in 4 task-list chunks (each chunk
-    receives the B panels again): the chunk products are the resident
-    product's blocks, bitwise."""
+@pytest.mark.parametrize("L", [32, 64, 128])
+def test_broadcast_row_chunks_bitwise(ctx, L):
+    """Broadcast transport through spg_spamm_panels with the task budget set
+    so the library splits the rows into 4 task-list chunks (each chunk
+    receives the B panels again): C~ is the resident product, bitwise."""
     from paper_2005_10680_b200 import _native as nat
     from paper_2005_10680_b200.inputs import log_grid
     from paper_2005_10680_b200.sharded import DistributedOperands
-    n, L = 2048, 64
+    n = 2048
     A = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 1, 1e-10)
     B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10)
+    ref, sref, _ = nat.spamm_with_error_control(ctx, A, B, 1e-6, log_grid(32))
     ops = DistributedOperands(ctx, A, B, 0, 0, lambda arrays: [arrays])
 
     def fetch(r0, r1, owner, buf, count, stream):
         nat.gather_rows(B, r0, r1, buf.data_ptr(), count, stream.cuda_stream)
 
-    pieces, st, bounds = ops.controlled_product(1e-6, log_grid(32), fetch, panel_rows=4,
-                                                row_chunks=4)
-    ref, sref, _ = nat.spamm_with_error_control(ctx, A, B, 1e-6, log_grid(32))
+    nat.set_task_budget(ctx, -(-40 * sref["spamm"]["candidates"] // 4))
+    try:
+        C, st, bounds = ops.controlled_product(1e-6, log_grid(32), fetch, panel_rows=4)
+    finally:
+        nat.set_task_budget(ctx, 0)
     assert st["spamm"]["survivors"] == sref["spamm"]["survivors"]
-    got = [p.download() for p in pieces]
-    r = np.concatenate([g[0] for g in got])
-    c = np.concatenate([g[1] for g in got])
-    p = np.concatenate([g[2] for g in got])
-    r0, c0, p0, _ = ref.download()
-    k, k0 = np.lexsort((c, r)), np.lexsort((c0, r0))
-    assert np.array_equal(r[k], r0[k0]) and np.array_equal(c[k], c0[k0])
-    assert bits_equal(p[k], p0[k0])
+    r, c, p, nr = C.download()
+    r0, c0, p0, n0 = ref.download()
+    assert np.array_equal(r, r0) and np.array_equal(c, c0)
+    assert bits_equal(p, p0) and bits_equal(nr, n0)
     assert st["panel_bytes"] == 4 * int(ops.B_norms.nnz_blocks) * L * L * 8
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L", [32, 64, 128])
+def test_resident_product_row_chunks_bitwise(ctx, L):
+    """spg_spamm / spg_spamm_with_error_control with a task budget too small
+    for the task list: the library runs the product in row chunks (super
+    blocks at L = 32, sub-products at L = 128 included) -- bitwise the same C,
+    same stats."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    n = 2048
+    A = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 1, 1e-10)
+    B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 2, 1e-10)
+    C0, s0, b0 = nat.spamm_with_error_control(ctx, A, B, 1e-6, log_grid(32))
+    E0, _ = nat.multiply_exact(ctx, A, B)
+    for budget in (40 * s0["spamm"]["candidates"] // 3, 4096):
+        nat.set_task_budget(ctx, budget)
+        try:
+            C1, s1, b1 = nat.spamm_with_error_control(ctx, A, B, 1e-6, log_grid(32))
+            E1, _ = nat.multiply_exact(ctx, A, B)
+        finally:
+            nat.set_task_budget(ctx, 0)
+        assert bits_equal(b0, b1) and s0["tau"] == s1["tau"]
+        for k in ("survivors", "output_blocks", "candidates"):
+            assert s0["spamm"][k] == s1["spamm"][k]
+        for X, Y in ((C0, C1), (E0, E1)):
+            x, y = X.download(), Y.download()
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1])
+            assert bits_equal(x[2], y[2]) and bits_equal(x[3], y[3])
 
 
 @pytest.mark.gpu

@@ -10,9 +10,10 @@ runs everything rank `rank` of those 8 would do, on one GPU:
     the global norm-only matrices built from them;
   * the rank's sweep share (spg_cse_shard), the other ranks' partials (what
     the partial all-gather delivers), spg_cse_finish -> bounds, tau;
-  * the rank's rows of C~ in 2^c row sub-chunks (task list <= 1/2^c of the
-    rank's), B arriving in block-row panels -- generated on the device here,
-    where on 8 GPUs the owner would broadcast them.
+  * the rank's rows of C~ through ONE C-ABI call (spg_spamm_panels), which
+    row-chunks the task list itself when it would not fit, B arriving in
+    block-row panels through its fetch callback -- generated on the device
+    here, where on 8 GPUs the owner would broadcast them.
 A's rows stay resident (the rank's own shard).  The single-GPU sweep of the
 whole problem runs too, and its bounds must equal the sharded ones bit for bit.
 One JSON line per delta.
@@ -32,11 +33,11 @@ import time
 import sys
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
 from paper_2005_10680_b200 import _native as nat  # noqa: E402
 from paper_2005_10680_b200.inputs import log_grid  # noqa: E402
-from paper_2005_10680_b200.sharded import (leaf_table, merge_tables, panel_schedule,  # noqa: E402
-                                           run_panels)
+from paper_2005_10680_b200.sharded import leaf_table, merge_tables  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4, choices=[4, 5])
@@ -45,7 +46,8 @@ ap.add_argument("--leaf", type=int, default=64)
 ap.add_argument("--rank", type=int, default=0)
 ap.add_argument("--ranks", type=int, default=8)
 ap.add_argument("--panel-rows", type=int, default=None)
-ap.add_argument("--row-chunks", type=int, default=8)
+ap.add_argument("--task-budget", type=float, default=0,
+                help="task-list bytes before the library row-chunks a product (0: auto)")
 ap.add_argument("--tau-lo", type=float, default=None)
 ap.add_argument("--deltas", default=None)
 ap.add_argument("--all-ranks", action="store_true",
@@ -63,16 +65,15 @@ deltas = [float(x) for x in (args.deltas or ("1e-8,1e-6,1e-4" if cfg5 else "1e-6
 # panel (config 5, L = 64, delta = 1e-4: 22.7 TFLOP/s with 128-row panels,
 # 28.4 with 512-row panels)
 panel_rows = args.panel_rows or max(8, (24 << 30) // (N * L * 8))
-rank, ranks, row_chunks = args.rank, args.ranks, args.row_chunks
+rank, ranks = args.rank, args.ranks
 ELL, DENS, SITE, SEED_A, SEED_B, DROP = 4.0, 0.1, 2005, 10680, 10681, 1e-10
 level = ranks.bit_length() - 1
-c = row_chunks.bit_length() - 1
-assert (1 << level) == ranks and (1 << c) == row_chunks
+assert (1 << level) == ranks
 
 ctx = nat.Context(0)
 base = {"workload": f"cfg{args.config}-cluster3d-N{N}-L{L}-ell{ELL}", "rank": rank,
         "ranks": ranks, "n_taus": NT, "tau_grid": [1e-2, tau_lo], "panel_rows": panel_rows,
-        "row_chunks": row_chunks}
+        "task_budget": args.task_budget or "auto"}
 t0 = time.perf_counter()
 sA = nat.synth_cluster_scale(ctx, N, ELL, DENS, SITE, SEED_A)
 sB = nat.synth_cluster_scale(ctx, N, ELL, DENS, SITE, SEED_B)
@@ -119,16 +120,18 @@ base["sharded_bounds_equal_one_gpu"] = bool(np.array_equal(full.view(np.uint64),
 base["bound_at_smallest_tau"] = float(bounds[-1])
 
 
-def fetch(r0, r1, owner, buf, count, stream):
-    # the owner's broadcast on 8 GPUs; here the panel is generated in place
+def cfetch(r0, r1, dst, count, stream):
+    # spg_spamm_panels' callback: the owner's broadcast on 8 GPUs; here the
+    # panel is generated in place and its leaves gathered into dst on `stream`
     Bp = nat.synth_cluster_device_rows_scaled(ctx, N, L, ELL, DENS, SITE, SEED_B, DROP, sB, r0, r1)
     ctx.synchronize()
-    nat.gather_rows(Bp, r0, r1, buf.data_ptr(), count, stream.cuda_stream)
-    stream.synchronize()
+    nat.gather_rows(Bp, r0, r1, dst, count, stream)
+    torch.cuda.ExternalStream(stream).synchronize()  # before Bp's memory is reused
     Bp.free()
 
 
-sched = panel_schedule(N, L, 0, panel_rows)
+if args.task_budget:
+    nat.set_task_budget(ctx, args.task_budget)
 for rk in run_ranks:
     if A_local is None:
         A_local = nat.synth_cluster_device_rows_scaled(ctx, N, L, ELL, DENS, SITE, SEED_A, DROP, sA,
@@ -150,15 +153,13 @@ for rk in run_ranks:
         tot = {"candidates": 0, "survivors": 0, "flops": 0.0, "ms_gemm": 0.0, "ms_tasklist": 0.0,
                "ms_finalize": 0.0, "output_blocks": 0}
         t3 = time.perf_counter()
-        for sub in range(row_chunks):
-            plan = nat.Plan(ctx, A_local, B_norms, tau, level + c, (rk << c) + sub,
-                            a_norms=A_norms)
-            run_panels(ctx, plan, sched, fetch, L)
-            C, st = plan.finish()
-            plan.free()
-            for key in tot:
-                tot[key] += st[key]
-            C.free()
+        # one C-ABI call: the library sizes the task-list row chunks itself
+        # (spg_context_set_task_budget; ~6e9 products per rank do not fit one)
+        C, st = nat.spamm_panels(ctx, A_local, B_norms, tau, cfetch, level, rk, panel_rows,
+                                 rows_per, a_norms=A_norms)
+        for key in tot:
+            tot[key] += st[key]
+        C.free()
         ctx.synchronize()
         out["product_wall_s"] = round(time.perf_counter() - t3, 2)
         out.update({k2: (round(v, 1) if isinstance(v, float) else v) for k2, v in tot.items()})
