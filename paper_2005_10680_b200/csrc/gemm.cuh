@@ -229,210 +229,6 @@ static __global__ void leaf_gemm_generic(const double* __restrict__ A, const dou
 }
 
 // ---------------------------------------------------------------------------
-// K5 v3: warp-specialised TMA pipeline (sm_100a).
-//
-// Warp 0 is the producer: for every (surviving product, k-chunk) step it waits
-// until the stage is free (empty mbarrier), arms the stage's full mbarrier
-// with the byte count and issues TMA bulk copies (cp.async.bulk, SASS UBLKCP)
-// -- one per leaf column: KC columns of A (L doubles each) and L column
-// pieces of B (KC doubles each) -- straight into the padded, bank-conflict-
-// free layout.  Warps 1..4 are consumers, each owning a 32x32 tile of the
-// 64x64 output block (16 DMMA.8x8x4 per 8 fragment loads), releasing each
-// stage with one elected arrive.  The CTA is persistent over output blocks,
-// so the producer streams the next block's operands while the consumers run
-// the epilogue of the current one.  No __syncthreads in the main loop.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                             uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <int NSTAGE>
-struct TmaGemmCfg {
-  static constexpr int L = 64;
-  static constexpr int KC = 32;
-  static constexpr int AS = L + 4;   // == 4 (mod 16)
-  static constexpr int BS = KC + 4;  // == 4 (mod 16)
-  static constexpr int A_STAGE = KC * AS;
-  static constexpr int B_STAGE = L * BS;
-  static constexpr int STAGE = A_STAGE + B_STAGE;
-  static constexpr int CHUNKS = L / KC;
-  static constexpr int kConsumers = 4;
-  static constexpr int kThreads = 32 * (kConsumers + 1);
-  static constexpr uint32_t kStageBytes = sizeof(double) * (KC * L + L * KC);
-  // stages, then per stage: full + empty mbarrier and a 16-byte tag
-  static constexpr size_t kSmemBytes = sizeof(double) * NSTAGE * STAGE + 32 * NSTAGE + 16;
-};
-
-// Stage tag written by the producer before it arms the stage: the output
-// block the stage belongs to, and whether it is the block's last step
-// (block = -1: no more work).
-struct StageTag {
-  int64_t block;
-  int32_t last;
-  int32_t pad;
-};
-
-template <int NSTAGE>
-__global__ void __launch_bounds__(TmaGemmCfg<NSTAGE>::kThreads, (NSTAGE <= 3) ? 2 : 1)
-    leaf_gemm_tma64(const double* __restrict__ A, const double* __restrict__ B,
-                    const int2* __restrict__ pairs, const int64_t* __restrict__ out_offset,
-                    int64_t n_out, double* __restrict__ C,
-                    unsigned long long* __restrict__ next_block) {
-  using Cfg = TmaGemmCfg<NSTAGE>;
-  constexpr int L = Cfg::L, KC = Cfg::KC;
-  constexpr int64_t LL = static_cast<int64_t>(L) * L;
-  extern __shared__ __align__(128) double smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * Cfg::STAGE);
-  uint64_t* empty = full + NSTAGE;
-  StageTag* tags = reinterpret_cast<StageTag*>(empty + NSTAGE);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NSTAGE; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::kConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {
-    // ---------------- producer: output blocks handed out in Morton order by a
-    // global counter, so the blocks in flight across the GPU stay a compact
-    // window (their A block-rows and B block-columns stay in L2)
-    int stage = 0;
-    uint32_t phase = 0;
-    for (;;) {
-      int64_t o = 0;
-      if (lane == 0) o = static_cast<int64_t>(atomicAdd(next_block, 1ull));
-      o = __shfl_sync(0xffffffffu, o, 0);
-      if (o >= n_out) {
-        mbar_wait(&empty[stage], phase ^ 1u);
-        if (lane == 0) {
-          tags[stage].block = -1;
-          mbar_arrive(&full[stage]);
-        }
-        break;
-      }
-      const int64_t beg = out_offset[o], end = out_offset[o + 1];
-      for (int64_t sv = beg; sv < end; ++sv) {
-        const int2 pr = __ldg(pairs + sv);
-        const double* Ablk = A + static_cast<int64_t>(pr.x) * LL;
-        const double* Bblk = B + static_cast<int64_t>(pr.y) * LL;
-#pragma unroll 1
-        for (int c = 0; c < Cfg::CHUNKS; ++c) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          double* As = smem + stage * Cfg::STAGE;
-          double* Bs = As + Cfg::A_STAGE;
-          if (lane == 0) {
-            tags[stage].block = o;
-            tags[stage].last = (sv + 1 == end) && (c + 1 == Cfg::CHUNKS);
-            mbar_arrive_expect_tx(&full[stage], Cfg::kStageBytes);
-          }
-          __syncwarp();
-          // A(:, c*KC + kk): contiguous column of L doubles
-          for (int kk = lane; kk < KC; kk += 32)
-            tma_bulk_g2s(As + kk * Cfg::AS, Ablk + static_cast<int64_t>(c * KC + kk) * L,
-                         L * sizeof(double), &full[stage]);
-          // B(c*KC : c*KC+KC, j): KC contiguous doubles of column j
-          for (int j = lane; j < L; j += 32)
-            tma_bulk_g2s(Bs + j * Cfg::BS, Bblk + static_cast<int64_t>(j) * L + c * KC,
-                         KC * sizeof(double), &full[stage]);
-          if (++stage == NSTAGE) {
-            stage = 0;
-            phase ^= 1u;
-          }
-        }
-      }
-    }
-  } else {
-    // ---------------- consumers: 32x32 tile each
-    const int cw = warp - 1;
-    const int m0 = (cw & 1) * 32, n0 = (cw >> 1) * 32;
-    const int g = lane >> 2, t = lane & 3;
-    const int pg = perm8(g);
-    int stage = 0;
-    uint32_t phase = 0;
-    double acc[4][4][2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (;;) {
-      mbar_wait(&full[stage], phase);
-      const int64_t o = tags[stage].block;
-      if (o < 0) break;
-      const bool last = tags[stage].last != 0;
-      const double* As = smem + stage * Cfg::STAGE;
-      const double* Bs = As + Cfg::A_STAGE;
-#pragma unroll
-      for (int ks = 0; ks < KC / 4; ++ks) {
-        double a[4], b[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = As[(4 * ks + t) * Cfg::AS + m0 + 8 * i + pg];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = Bs[(n0 + 8 * j + pg) * Cfg::BS + 4 * ks + t];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma_884(acc[i][j], a[i], b[j]);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == NSTAGE) {
-        stage = 0;
-        phase ^= 1u;
-      }
-      if (last) {
-        double* Cblk = C + o * LL;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int row = m0 + 8 * i + pg;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int col = n0 + 8 * j + perm8(2 * t + e);
-              Cblk[static_cast<int64_t>(col) * L + row] = acc[i][j][e];
-              acc[i][j][e] = 0.0;
-            }
-          }
-      }
-    }
-  }
-}
-
-
-// ---------------------------------------------------------------------------
 // L = 32 super-block GEMM: one CTA per 2x2 group of output blocks
 // (rows 2I, 2I+1 x cols 2J, 2J+1), warp s = 2 ri + cj owning block
 // (2I+ri, 2J+cj) as a 32x32 tile (16 DMMA per 8 fragment loads).  Each

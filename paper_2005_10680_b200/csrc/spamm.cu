@@ -243,95 +243,29 @@ void launch_dmma(spg_context* ctx, const double* A, const double* B, const int2*
   SPG_CHECK_LAUNCH(ctx);
 }
 
-template <int NSTAGE>
-void launch_tma64(spg_context* ctx, const double* A, const double* B, const int2* pairs,
-                  const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st) {
-  using Cfg = TmaGemmCfg<NSTAGE>;
-  auto kern = leaf_gemm_tma64<NSTAGE>;
-  SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(Cfg::kSmemBytes)));
-  int per_sm = 1;
-  SPG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads,
-                                                         Cfg::kSmemBytes));
-  const int64_t grid = std::min<int64_t>(n_out, static_cast<int64_t>(ctx->sm_count) *
-                                                    std::max(per_sm, 1));
-  DevBuf<unsigned long long> counter(1, ctx);
-  SPG_CUDA(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned long long), st));
-  kern<<<static_cast<unsigned>(grid), Cfg::kThreads, Cfg::kSmemBytes, st>>>(
-      A, B, pairs, out_offset, n_out, C, counter.get());
-  SPG_CHECK_LAUNCH(ctx);
-}
-
-int gemm_variant() {
-  static const int v = [] {
-    const char* e = std::getenv("SPG_GEMM");  // developer switch (variants below)
-    return e ? std::atoi(e) : 4;
-  }();
-  return v;
-}
-
 void run_gemm(spg_context* ctx, int L, const double* A, const double* B, const int2* pairs,
               const int64_t* out_offset, int64_t n_out, double* C, cudaStream_t st = nullptr,
               const int64_t* out_end = nullptr, int accumulate = 0,
               const double* const* btab = nullptr, const int32_t* order = nullptr) {
   if (n_out == 0) return;
   if (!st) st = ctx->stream;
-  if ((out_end || accumulate || btab) && L == 64 && gemm_variant() == 3)
-    fail(SPG_EINVAL, "panels / leaf tables are not supported by the TMA variant");
-  if (L == 64 && gemm_variant() == 3) {
-    launch_tma64<3>(ctx, A, B, pairs, out_offset, n_out, C, st);
-    return;
-  }
-  if (L == 64 && gemm_variant() == 4) {  // 4 warps x 32x32, 2 stages, 3 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab,
-                                   order);
-    return;
-  }
-  if (L == 64 && gemm_variant() == 5) {  // 4 warps x 32x32, 3 stages, 2 CTAs/SM
-    launch_dmma<64, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate,
-                                   btab, order);
-    return;
-  }
-  if (L == 64 && gemm_variant() == 6) {  // 4 warps x 32x32, KC=16, 4 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-    return;
-  }
-  if (L == 64 && gemm_variant() == 8) {  // 4 warps x 32x32, KC=16, 3 stages, 3 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-    return;
-  }
-  if (L == 64 && gemm_variant() == 7) {  // 4 warps x 32x32, KC=16, 6 stages, 2 CTAs/SM
-    launch_dmma<64, 16, 32, 32, 6>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-    return;
-  }
   switch (L) {
     case 32: {
-      static const int v32 = [] {
-        const char* e = std::getenv("SPG_GEMM32");  // developer switch for the L=32 tiling
-        return e ? std::atoi(e) : 6;
-      }();
-      if (v32 == 1) launch_dmma<32, 32, 16, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v32 == 2) launch_dmma<32, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v32 == 3) launch_dmma<32, 32, 32, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v32 == 4) launch_dmma<32, 16, 32, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v32 == 6) launch_dmma<32, 32, 32, 16, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v32 == 7) launch_dmma<32, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v32 == 8) launch_dmma<32, 32, 16, 16, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else launch_dmma<32, 32, 16, 8, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
+      // per-block L = 32 tiling (the super-block kernel is the default where
+      // it applies; SPG_GEMM32=6 forces this one)
+      launch_dmma<32, 32, 32, 16, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end,
+                                     accumulate, btab, order);
       break;
     }
-    case 64:
-      launch_dmma<64, 32, 32, 16, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
+    case 64:  // 4 warps x 32x32 tiles, 2 stages, 3 CTAs/SM
+      launch_dmma<64, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end,
+                                     accumulate, btab, order);
       break;
     case 128: {
-      static const int v128 = [] {
-        const char* e = std::getenv("SPG_GEMM128");  // developer switch for the L=128 tiling
-        return e ? std::atoi(e) : 3;
-      }();
-      if (v128 == 2) launch_dmma<128, 16, 64, 32, 3>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v128 == 3) launch_dmma<128, 32, 64, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else if (v128 == 4) launch_dmma<128, 32, 32, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
-      else launch_dmma<128, 16, 64, 32, 4>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end, accumulate, btab, order);
+      // L = 128 kernel (the L = 64 sub-products are the default where they
+      // apply; SPG_GEMM128=3 forces this one)
+      launch_dmma<128, 32, 64, 32, 2>(ctx, A, B, pairs, out_offset, n_out, C, st, out_end,
+                                      accumulate, btab, order);
       break;
     }
     default: {

@@ -210,13 +210,13 @@ def test_sweep_wide_breakpoint_ranges(ctx, port, n_taus):
 
 @pytest.mark.parametrize("env", [{"SPG_CSE_LISTS": "1"}, {"SPG_CSE_FOLD": "2"},
                                  {"SPG_CSE_FOLD": "2", "SPG_CSE_LISTS": "1"},
-                                 {"SPG_CSE_FOLD": "0"}, {"SPG_CSE": "6"},
+                                 {"SPG_CSE_FOLD": "0"}, {"SPG_CSE": "4"},
                                  {"SPG_CSE_SYNC": "1", "SPG_CSE_LISTS": "1"},
-                                 {"SPG_CSE_SYNC": "1", "SPG_CSE_LISTS": "1", "SPG_CSE": "6"}])
+                                 {"SPG_CSE_SYNC": "1", "SPG_CSE_LISTS": "1", "SPG_CSE": "4"}])
 def test_sweep_paths_in_subprocesses(port, env):
     """Every sweep path (pair lists instead of dense enumeration, level s-1
-    folded into the tile CTAs or not, the v6 kernel, the host-synchronised
-    list path) gives the oracle's bounds
+    folded into the tile CTAs or not, the general tile kernel of grids the
+    bucket table cannot hold, the host-synchronised list path) gives the oracle's bounds
     bit for bit; the path is fixed per process, so each runs in a child."""
     import os
     import subprocess
@@ -237,8 +237,7 @@ def test_sweep_paths_in_subprocesses(port, env):
         assert got[name] == want, (env, name)
 
 
-@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_GEMM32": "3"},
-                                 {"SPG_GEMM128": "3"}])
+@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_GEMM128": "3"}])
 def test_gemm_paths_in_subprocesses(env):
     """Leaf-GEMM variants that keep every block's products in ascending k and
     the same DMMA k-steps give C~ bit for bit equal to each other: the L = 32
