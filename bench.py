@@ -448,6 +448,10 @@ def run_ours(args, dist):
                           f"no flush: {A_bytes / 1e6:.0f} MB of leaves")},
         "pct_peak": round(100.0 * value / DMMA_PEAK_TFLOPS, 2),
         "sweep_ms": round(cse_ms, 4),
+        # the reference's cse_seconds is host wall time (error_control.cpp:207-209): launch
+        # overhead and the bound copy included
+        "sweep_wall_ms": (round(1e3 * sum(s["cse_seconds"] for s in stats) / len(stats), 4)
+                          if all(s.get("cse_seconds") for s in stats) else None),
         "tau": st["tau"], "tau_index": st["tau_index"], "bound": st["bound"],
         "candidates": int(cand), "survivors": int(surv),
         "skipped_fraction": round(1.0 - surv / max(cand, 1), 6),

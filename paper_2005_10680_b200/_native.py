@@ -227,6 +227,22 @@ EXPORTED_SYMBOLS = tuple(_SIGNATURES)
 _lib = None
 
 
+def _prefer_torch_nccl():
+    """Point the library's NCCL dlopen (SPG_NCCL_LIB) at the NCCL torch itself
+    links (the nvidia-nccl wheel), so one process holds one libnccl.so.2: a
+    communicator created before `import torch` would otherwise load the system
+    NCCL under the same soname, and torch's newer symbols would not resolve."""
+    if os.environ.get("SPG_NCCL_LIB"):
+        return
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for root in (spec.submodule_search_locations or []) if spec else []:
+        cand = Path(root) / "nccl" / "lib" / "libnccl.so.2"
+        if cand.exists():
+            os.environ["SPG_NCCL_LIB"] = str(cand)
+            return
+
+
 def lib():
     """Load the in-tree library (raises if it was not built)."""
     global _lib
@@ -234,6 +250,7 @@ def lib():
         if not LIB_PATH.exists():
             raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
                               "(the CUDA path has no fallback)")
+        _prefer_torch_nccl()
         handle = C.CDLL(str(LIB_PATH))
         for name, (res, args) in _SIGNATURES.items():
             fn = getattr(handle, name)
