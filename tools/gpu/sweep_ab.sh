@@ -1,7 +1,7 @@
-# v9 vs v8 sweep: parity suites for the sweep, A/B timings (bits must match), SPG_TRACE phases, ncu of the v9 tile kernel
+# sweep kernel iteration: parity suites for the sweep, timings (bits must match v8's digests), ncu of the tile kernel at 32 and 128 tau
 set -x
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_large.py tests/test_gpu_reference_cases.py -x -q > gpurun_out/sweep_tests.log 2>&1; echo rc=$? >> gpurun_out/sweep_tests.log
 timeout 300 python tools/sweep_ab.py 10 > gpurun_out/ab_v9.jsonl 2> gpurun_out/ab_v9.err
-SPG_CSE_V8=1 timeout 300 python tools/sweep_ab.py 10 > gpurun_out/ab_v8.jsonl 2> gpurun_out/ab_v8.err
 SPG_TRACE=1 timeout 300 python tools/sweep_ab.py 2 > /dev/null 2> gpurun_out/ab_v9_trace.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:cse_tile9 -c 1 -o gpurun_out/cse9_32 -f python tools/cse_probe.py 32 1 > gpurun_out/cse9_ncu.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:cse_tile9 -c 1 -o gpurun_out/cse9_128 -f python tools/cse_probe.py 128 1 1e-14 > gpurun_out/cse9_128.log 2>&1
