@@ -1,6 +1,6 @@
 """tau-sweep A/B on the cfg2 matrix: host wall time of spg_cse (bounds on the
 host) over several grids, plus a digest of the bound bits so two builds or two
-kernel variants (SPG_CSE_V8=1) can be compared bit for bit.
+kernel versions can be compared bit for bit.
     python tools/sweep_ab.py [reps]   -> one JSON line per grid"""
 import hashlib
 import json
