@@ -92,6 +92,9 @@ int spg_context_launch_count(spg_context* ctx, int64_t* launches);
  * in 2^c row chunks, one task list at a time, into one C; bitwise the same C
  * (same products, same per-block k order). */
 int spg_context_set_task_budget(spg_context* ctx, int64_t bytes);
+/* Return the context's cached (freed) device blocks to the driver; live
+ * matrices are untouched.  Allocation failures trim by themselves first. */
+int spg_context_trim(spg_context* ctx);
 
 /* ---- matrices (quadtree.hpp / quadtree.cpp) ------------------------------ */
 /* Replaces QuadTreeMatrix::from_coordinates at leaf granularity

@@ -180,6 +180,7 @@ _SIGNATURES = {
     "spg_matrix_rows": (C.c_int, [_vp, _dp, _dp]),
     "spg_matrix_gershgorin": (C.c_int, [_vp, _dp, _dp]),
     "spg_context_set_task_budget": (C.c_int, [_vp, C.c_int64]),
+    "spg_context_trim": (C.c_int, [_vp]),
     "spg_spamm_panels": (C.c_int, [_vp, _vp, _vp, _vp, C.c_double, C.c_int32, C.c_int32,
                                    C.c_int32, C.c_int32, _vp, _vp, C.POINTER(_vp), _vp]),
     "spg_comm_unique_id": (C.c_int, [_vp]),
@@ -309,6 +310,10 @@ class Context:
 
     def synchronize(self):
         _check(lib().spg_context_synchronize(self._h))
+
+    def trim(self):
+        """Return cached device blocks to the driver (spg_context_trim)."""
+        _check(lib().spg_context_trim(self._h))
 
     def launch_count(self) -> int:
         n = C.c_int64(0)

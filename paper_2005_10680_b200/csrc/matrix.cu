@@ -534,6 +534,14 @@ int spg_context_set_task_budget(spg_context* ctx, int64_t bytes) {
   SPG_API_END
 }
 
+int spg_context_trim(spg_context* ctx) {
+  SPG_API_BEGIN
+  if (!ctx) fail(SPG_EINVAL, "null context");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  ctx->pool.trim(ctx->stream);
+  SPG_API_END
+}
+
 int spg_context_launch_count(spg_context* ctx, int64_t* launches) {
   SPG_API_BEGIN
   if (!ctx || !launches) fail(SPG_EINVAL, "null argument");
