@@ -820,8 +820,14 @@ void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_mat
 // spg_context_set_task_budget): 2^c sub-shards of `sh`, one task list at a
 // time.  ~40 B per candidate bounds the build's peak (triples, masks, keys
 // and their sorted copy, pairs).
+// Row-chunk bits for a product whose task list would not fit: peak device
+// bytes per candidate leaf product of a plan (keys, pairs, the radix sort's
+// double buffers and temp storage) -- about 40 B, and 96 B when the L = 32
+// super-block re-keying (its own sort of 64-bit keys and values) follows --
+// against half of the free memory (plus this context's cached blocks) left
+// after `reserve` bytes for the output, whose chunks accumulate.
 int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard sh,
-               int max_bits) {
+               int max_bits, bool super32, int64_t reserve) {
   if (max_bits <= 0) return 0;
   int64_t budget = ctx->task_budget;
   if (budget <= 0) {
@@ -829,13 +835,24 @@ int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard
     SPG_CUDA(cudaMemGetInfo(&fr, &tot));
     size_t cached = 0;
     for (const auto& kv : ctx->pool.free_blocks) cached += kv.first;
-    budget = static_cast<int64_t>((fr + cached) / 2);
+    const int64_t avail = static_cast<int64_t>(fr + cached) - std::max<int64_t>(reserve, 0);
+    budget = std::max<int64_t>(avail / 2, static_cast<int64_t>(fr / 8));
   }
-  const double need = 40.0 * static_cast<double>(count_candidates(ctx, a, b, sh));
+  const double per_cand = super32 ? 96.0 : 40.0;
+  const double need = per_cand * static_cast<double>(count_candidates(ctx, a, b, sh));
   int c = 0;
   while (c < max_bits && need / static_cast<double>(int64_t(1) << c) > static_cast<double>(budget))
     ++c;
   return c;
+}
+
+// upper bound of an output's payload bytes: the shard's block rows x all
+// block columns
+int64_t output_bytes_bound(const spg_matrix* a, Shard sh) {
+  const int64_t nb = (a->dimension + a->leaf - 1) / a->leaf;
+  const int64_t rows = std::max<int64_t>(1, ((int64_t(1) << a->depth) >> sh.level));
+  const int64_t LL = static_cast<int64_t>(a->leaf) * a->leaf;
+  return std::min(rows, nb) * nb * LL * static_cast<int64_t>(sizeof(double));
 }
 
 void gemm_plan(spg_context* ctx, int depth, int L, const Plan& plan, bool super32,
@@ -941,7 +958,8 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
   const int64_t LL = static_cast<int64_t>(L) * L;
   const bool super32 = L == 32 && !host && super32_enabled();
   if (!host) {  // super blocks pair rows 2I, 2I+1: a chunk keeps >= 2 rows for them
-    const int c = chunk_bits(ctx, a, b, shard, a->depth - shard.level - (super32 ? 1 : 0));
+    const int c = chunk_bits(ctx, a, b, shard, a->depth - shard.level - (super32 ? 1 : 0),
+                             super32, output_bytes_bound(a, shard));
     if (c > 0) return spamm_device_chunked(ctx, a, b, tau, skip_test, stats, shard, c, super32);
   }
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
@@ -1329,7 +1347,10 @@ spg_matrix* spamm_panels_device(spg_context* ctx, std::unique_lock<std::mutex>& 
   int64_t cap = 0;
   for (const auto& pr : panels) cap = std::max(cap, rs[pr.second] - rs[pr.first]);
   const spg_matrix* an = a_norms ? a_norms : a;
-  const int c = chunk_bits(ctx, an, b, sh, a->depth - sh.level);
+  // super blocks pair rows 2I, 2I+1: a chunk keeps >= 2 rows for them
+  const bool super32 = a->leaf == 32 && super32_enabled();
+  const int c = chunk_bits(ctx, an, b, sh, a->depth - sh.level - (super32 ? 1 : 0), super32,
+                           output_bytes_bound(a, sh));
   std::vector<spg_matrix*> parts;
   struct Parts {
     std::vector<spg_matrix*>& v;
