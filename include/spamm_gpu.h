@@ -87,7 +87,8 @@ int spg_context_synchronize(spg_context* ctx);
 int spg_context_launch_count(spg_context* ctx, int64_t* launches);
 /* Products larger than the device's memory (the reference's spamm_multiply
  * has no size cap, multiply.cpp:109-116): when a product's task list (at
- * most ~40 B per candidate leaf product) would exceed `bytes` -- 0 (default):
+ * most ~40 B per candidate leaf product, ~96 B for L = 32 leaves, whose
+ * super-block re-keying sorts again) would exceed `bytes` -- 0 (default):
  * half of the free HBM plus the context's cached pool -- the product is run
  * in 2^c row chunks, one task list at a time, into one C; bitwise the same C
  * (same products, same per-block k order). */
