@@ -1,5 +1,14 @@
-# sweep iteration: sweep parity suites, grid timings (digests must not change), ncu at 128 tau
+# sweep iteration: sweep parity suites + the large pins, grid timings (digests must not change)
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_large.py tests/test_gpu_reference_cases.py -x -q > gpurun_out/sweep_tests.log 2>&1; echo rc=$? >> gpurun_out/sweep_tests.log
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_large.py tests/test_gpu_reference_cases.py tests/test_gpu_pins.py tests/test_distributed_panels.py -x -q --durations=8 > gpurun_out/sweep_tests.log 2>&1; echo rc=$? >> gpurun_out/sweep_tests.log
 timeout 300 python tools/sweep_ab.py 10 > gpurun_out/ab_v9.jsonl 2> gpurun_out/ab_v9.err
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:cse_tile9 -c 1 -o gpurun_out/cse9_128 -f python tools/cse_probe.py 128 1 1e-14 > gpurun_out/cse9_128.log 2>&1
+SPG_TRACE=1 timeout 600 python -c "
+import sys; sys.path.insert(0, 'tests')
+from large_cases import GpuCase
+from paper_2005_10680_b200 import _native as nat
+import time
+ctx = nat.Context(0)
+g = GpuCase(ctx, 'cfg5-L32')
+for _ in range(2):
+    t0 = time.perf_counter(); b = nat.cse(ctx, g.A_norms, g.B_norms, g.taus); print('cfg5-L32 one-GPU sweep s', round(time.perf_counter() - t0, 3), flush=True)
+" > gpurun_out/cfg5_l32_sweep.log 2>&1
