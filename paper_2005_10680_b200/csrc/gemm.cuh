@@ -243,6 +243,16 @@ struct SuperEntry {
   int32_t a0, a1, b0, b1;  // A slots of rows 2I, 2I+1 at k; B slots of cols 2J, 2J+1
 };
 
+// kQuad: warp w owns the 16x16 quadrant (w >> 1, w & 1) of EACH of the four
+// blocks instead of one whole block, so every warp has the same work whatever
+// the entry mask (a warp owning a block the entry skips used to wait at the
+// barrier: 18 % of stall samples, DMMA pipe 86 % active at 55 % skipped).
+// A full mask shares each block row's A and block column's B fragments
+// between the two blocks using them (16 DMMA per 8 fragment loads); a partial
+// mask runs the present blocks one by one (4 DMMA per 4 loads).  Every output
+// element sees the same DMMA k-steps in the same order: bitwise the one-warp-
+// per-block variant (kQuad = false).
+template <bool kQuad>
 __global__ void __launch_bounds__(128, 3)
     leaf_gemm_super32(const double* __restrict__ A, const double* const* __restrict__ btab,
                       const SuperEntry* __restrict__ ent, const uint32_t* __restrict__ emask,
@@ -256,7 +266,8 @@ __global__ void __launch_bounds__(128, 3)
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3, pg = perm8(g);
-  const int ri = warp >> 1, cj = warp & 1;
+  const int ri = warp >> 1, cj = warp & 1;  // whole-block mode: the warp's block
+  const int qr = warp >> 1, qc = warp & 1;  // quadrant mode: the warp's quadrant
 
   for (int64_t sbi = blockIdx.x; sbi < n_sb; sbi += gridDim.x) {
     const int64_t sb = order ? order[sbi] : sbi;
@@ -265,7 +276,6 @@ __global__ void __launch_bounds__(128, 3)
     const int64_t beg = sb_beg[sb];
     const int64_t n = sb_end[sb] - beg;
     if (n == 0) continue;  // uniform per CTA
-    const int32_t o = sb_out[4 * sb + warp];
 
     auto load_stage = [&](const SuperEntry& en, uint32_t m, int stage) {
       double* st = smem + stage * STAGE;
@@ -288,17 +298,39 @@ __global__ void __launch_bounds__(128, 3)
       }
     };
 
+    // whole-block mode: acc[i][j] = the warp's block; quadrant mode: acc[b][2 i + j]
+    // with b the block, i, j < 2 the 8x8 tiles of the warp's quadrant
     double acc[4][4][2];
+    if constexpr (kQuad) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+      for (int bl = 0; bl < 4; ++bl) {
+        const int32_t ob = sb_out[4 * sb + bl];
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          acc[i][j][e] = (accumulate && o >= 0)
-                             ? C[static_cast<int64_t>(o) * LL +
-                                 static_cast<int64_t>(8 * j + perm8(2 * t + e)) * L + 8 * i + pg]
-                             : 0.0;
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              acc[bl][2 * i + j][e] =
+                  (accumulate && ob >= 0)
+                      ? C[static_cast<int64_t>(ob) * LL +
+                          static_cast<int64_t>(16 * qc + 8 * j + perm8(2 * t + e)) * L +
+                          16 * qr + 8 * i + pg]
+                      : 0.0;
+      }
+    } else {
+      const int32_t o = sb_out[4 * sb + warp];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            acc[i][j][e] = (accumulate && o >= 0)
+                               ? C[static_cast<int64_t>(o) * LL +
+                                   static_cast<int64_t>(8 * j + perm8(2 * t + e)) * L + 8 * i + pg]
+                               : 0.0;
+    }
 
     // entries are fetched one step ahead, so their global latency hides
     // behind a compute step (as pr_next in leaf_gemm_dmma)
@@ -324,8 +356,54 @@ __global__ void __launch_bounds__(128, 3)
         en_next = ent[beg + step + 2];
         m_next = emask[beg + step + 2];
       }
-      if ((m_step >> warp) & 1u) {
-        const double* st = smem + static_cast<int>(step & 1) * STAGE;
+      const double* st = smem + static_cast<int>(step & 1) * STAGE;
+      if constexpr (kQuad) {
+        if (m_step == 15u) {
+          // all four products: each block row's A fragments and each block
+          // column's B fragments loaded once for the two blocks sharing them
+          // (16 DMMA per 8 fragment loads, as the one-warp-per-block kernel)
+#pragma unroll
+          for (int ks = 0; ks < L / 4; ++ks) {
+            double a[2][2], b[2][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              a[0][i] = st[(4 * ks + t) * S + 16 * qr + 8 * i + pg];
+              a[1][i] = st[TILE + (4 * ks + t) * S + 16 * qr + 8 * i + pg];
+              b[0][i] = st[2 * TILE + (16 * qc + 8 * i + pg) * S + 4 * ks + t];
+              b[1][i] = st[3 * TILE + (16 * qc + 8 * i + pg) * S + 4 * ks + t];
+            }
+#pragma unroll
+            for (int bl = 0; bl < 4; ++bl)
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                  dmma_884(acc[bl][2 * i + j], a[bl >> 1][i], b[bl & 1][j]);
+          }
+        } else {
+        // a partial mask: one branch per block (a predicated DMMA would still
+        // occupy the pipe)
+#pragma unroll
+        for (int bl = 0; bl < 4; ++bl) {
+          if (!((m_step >> bl) & 1u)) continue;  // uniform per CTA
+          const double* As = st + (bl >> 1) * TILE;
+          const double* Bs = st + (2 + (bl & 1)) * TILE;
+#pragma unroll
+          for (int ks = 0; ks < L / 4; ++ks) {
+            double a[2], b[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              a[i] = As[(4 * ks + t) * S + 16 * qr + 8 * i + pg];
+              b[i] = Bs[(16 * qc + 8 * i + pg) * S + 4 * ks + t];
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) dmma_884(acc[bl][2 * i + j], a[i], b[j]);
+          }
+        }
+        }
+      } else if ((m_step >> warp) & 1u) {
         const double* As = st + ri * TILE;
         const double* Bs = st + (2 + cj) * TILE;
 #pragma unroll
@@ -344,19 +422,40 @@ __global__ void __launch_bounds__(128, 3)
     }
     cp_async_wait<0>();
     __syncthreads();
-    if (o >= 0) {
-      double* Cblk = C + static_cast<int64_t>(o) * LL;
+    if constexpr (kQuad) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int bl = 0; bl < 4; ++bl) {
+        const int32_t ob = sb_out[4 * sb + bl];
+        if (ob < 0) continue;
+        double* Cblk = C + static_cast<int64_t>(ob) * LL;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int row = 8 * i + pg;
+        for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int col = 8 * j + perm8(2 * t + e);
-            Cblk[static_cast<int64_t>(col) * L + row] = acc[i][j][e];
+          for (int j = 0; j < 2; ++j) {
+            const int row = 16 * qr + 8 * i + pg;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = 16 * qc + 8 * j + perm8(2 * t + e);
+              Cblk[static_cast<int64_t>(col) * L + row] = acc[bl][2 * i + j][e];
+            }
           }
-        }
+      }
+    } else {
+      const int32_t o = sb_out[4 * sb + warp];
+      if (o >= 0) {
+        double* Cblk = C + static_cast<int64_t>(o) * LL;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int row = 8 * i + pg;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int col = 8 * j + perm8(2 * t + e);
+              Cblk[static_cast<int64_t>(col) * L + row] = acc[i][j][e];
+            }
+          }
+      }
     }
   }
 }

@@ -623,14 +623,23 @@ void launch_super32(spg_context* ctx, const Super32& sp, const double* A,
                     const int64_t* end = nullptr, int accumulate = 0) {
   if (sp.n_sb == 0) return;
   constexpr size_t smem = 2 * 4 * 32 * 36 * sizeof(double);
-  SPG_CUDA(cudaFuncSetAttribute(leaf_gemm_super32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sp.n_sb, int64_t(1) << 30));
-  leaf_gemm_super32<<<grid, 128, smem, ctx->stream>>>(
-      A, btab, sp.ent.get(), sp.emask.get(), beg ? beg : sp.sb_offset.get(),
-      end ? end : sp.sb_offset.get() + 1, sp.sb_out.get(), sp.n_sb, C, sp.order.get(),
-      accumulate);
-  SPG_CHECK_LAUNCH(ctx);
+  auto go = [&](auto kern) {
+    SPG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(sp.n_sb, int64_t(1) << 30));
+    kern<<<grid, 128, smem, ctx->stream>>>(
+        A, btab, sp.ent.get(), sp.emask.get(), beg ? beg : sp.sb_offset.get(),
+        end ? end : sp.sb_offset.get() + 1, sp.sb_out.get(), sp.n_sb, C, sp.order.get(),
+        accumulate);
+    SPG_CHECK_LAUNCH(ctx);
+  };
+  // developer switch SPG_SUPER32_QUAD=0: one warp per block (the round-1 kernel)
+  static const bool quad = [] {
+    const char* e = std::getenv("SPG_SUPER32_QUAD");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (quad) go(leaf_gemm_super32<true>);
+  else go(leaf_gemm_super32<false>);
 }
 
 void run_super32(spg_context* ctx, int depth, const Plan& pl, const double* A,

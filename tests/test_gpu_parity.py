@@ -237,7 +237,7 @@ def test_sweep_paths_in_subprocesses(port, env):
         assert got[name] == want, (env, name)
 
 
-@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_GEMM128": "3"}])
+@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_SUPER32_QUAD": "0"}, {"SPG_GEMM128": "3"}])
 def test_gemm_paths_in_subprocesses(env):
     """Leaf-GEMM variants that keep every block's products in ascending k and
     the same DMMA k-steps give C~ bit for bit equal to each other: the L = 32
