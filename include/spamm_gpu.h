@@ -198,6 +198,13 @@ int spg_survivor_digest(spg_context* ctx, const spg_matrix* a, const spg_matrix*
 int spg_parity_audit(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                      int32_t ulps, int64_t* near_ties, int64_t* candidates);
 
+/* Self-test of the sweep kernels' branch-free square root (csrc/cse.cu
+ * sqrt_fast + its out-of-line slow path) against the correctly rounded
+ * sqrt.rn.f64 the reference's std::sqrt stands for (error_control.cpp:77):
+ * 2n seeded bit patterns over every exponent, sign and special value plus
+ * perfect squares +-1 ulp; *mismatches counts differing result bits. */
+int spg_selftest_sqrt(spg_context* ctx, int64_t n, uint64_t seed, int64_t* mismatches);
+
 /* ---- callers of the hot path (SURVEY.md 8f "next" row 1) ----------------- */
 /* truncate (error_control.hpp:59-62, error_control.cpp:174-201): remove whole
  * leaves greedily in ascending (norm, row-major position) order while the

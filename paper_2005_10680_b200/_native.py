@@ -133,6 +133,7 @@ _SIGNATURES = {
                                                        C.c_int64, _i32p, _i32p, _dp, _dp, _i64p,
                                                        _dp, C.POINTER(ControlledStats)]),
     "spg_parity_audit": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int32, _i64p, _i64p]),
+    "spg_selftest_sqrt": (C.c_int, [_vp, C.c_int64, C.c_uint64, _i64p]),
     "spg_matrix_trace": (C.c_int, [_vp, _dp]),
     "spg_matrix_nnz": (C.c_int, [_vp, _i64p]),
     "spg_matrix_axpby": (C.c_int, [_vp, C.c_double, _vp, C.c_double, _vp, C.POINTER(_vp)]),
@@ -746,6 +747,13 @@ def parity_audit(ctx: Context, a: Matrix, b: Matrix, tau: float, ulps: int = 4):
     _check(lib().spg_parity_audit(ctx.handle, a.handle, b.handle, tau, ulps, C.byref(t),
                                   C.byref(c)))
     return t.value, c.value
+
+
+def selftest_sqrt(ctx: Context, n: int, seed: int) -> int:
+    """Mismatching results of the sweep's branch-free sqrt vs sqrt.rn.f64 over 2n patterns."""
+    out = C.c_int64(-1)
+    _check(lib().spg_selftest_sqrt(ctx.handle, n, seed, C.byref(out)))
+    return out.value
 
 
 def trace(m: Matrix) -> float:

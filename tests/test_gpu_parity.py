@@ -208,6 +208,37 @@ def test_sweep_wide_breakpoint_ranges(ctx, port, n_taus):
     assert bits_equal(nat.cse(ctx, A, A, taus), port.cse(ta, ta, taus))
 
 
+def test_sweep_branch_free_sqrt_is_correctly_rounded(ctx):
+    """The tile kernels take square roots through the builtin's fast path with
+    one shared range check per group of evaluations (csrc/cse.cu sqrt_fast);
+    4e9 bit patterns over every exponent, sign and special value, and perfect
+    squares +-1 ulp, give sqrt.rn.f64's bits."""
+    from paper_2005_10680_b200 import _native as nat
+    assert nat.selftest_sqrt(ctx, 2_000_000_000, 20051068) == 0
+    assert nat.selftest_sqrt(ctx, 1000, 7) == 0
+
+
+@pytest.mark.parametrize("n_taus,scale", [(32, 1e-75), (32, 1e-78), (128, 1e-77), (64, 1e-150)])
+def test_sweep_tiny_norms_take_the_sqrt_slow_path(ctx, port, n_taus, scale):
+    """Norm products around 1e-150: their squares fall below 2^-970 (the range
+    the fast square root covers), into the subnormals, or underflow to zero."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    rng = np.random.default_rng(77)
+    n, L = 256, 4
+    nb = n // L
+    spread = np.repeat(np.repeat(10.0 ** rng.uniform(-6, 0, (nb, nb)), L, 0), L, 1)
+    da = rng.uniform(-1, 1, (n, n)) * spread * scale
+    db = rng.uniform(-1, 1, (n, n)) * spread.T * scale
+    la, lb = nat.dense_to_leaves(da, L), nat.dense_to_leaves(db, L)
+    A, B = nat.upload(ctx, n, L, *la), nat.upload(ctx, n, L, *lb)
+    ta, tb = port.build(n, L, *la), port.build(n, L, *lb)
+    taus = log_grid(n_taus, scale * scale * 10.0, scale * scale * 1e-12)
+    got, want = nat.cse(ctx, A, B, taus), port.cse(ta, tb, taus)
+    assert bits_equal(got, want)
+    assert scale < 1e-100 or np.count_nonzero(want) > 0
+
+
 @pytest.mark.parametrize("env", [{"SPG_CSE_LISTS": "1"}, {"SPG_CSE_FOLD": "2"},
                                  {"SPG_CSE_FOLD": "2", "SPG_CSE_LISTS": "1"},
                                  {"SPG_CSE_FOLD": "0"}, {"SPG_CSE": "4"},
