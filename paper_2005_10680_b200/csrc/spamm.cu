@@ -132,6 +132,251 @@ __global__ void triples_to_keys(const int32_t* __restrict__ I, const int32_t* __
             static_cast<uint32_t>(K[t]);
 }
 
+// ---- K4 without a sort: dense enumeration by output tile -------------------
+// The surviving products grouped by output block (Morton order) with k
+// ascending is exactly what a warp produces when it owns one 8 x 8 tile of
+// output blocks, T = (I, J) at level s = depth - 3, and walks K = 0 .. 2^s - 1
+// in order: a product (i, k, j) survives iff every ancestor pair of it passes
+// the rule (multiply.cpp:70-76: spamm_node returns at the first null or
+// skipped pair), so
+//   1. tl_valid: one flag per (T, K), the pair (I, K, J) and its ancestors of
+//      levels 0 .. s pass (and I lies in the shard's rows);
+//   2. tl_tile<count>: for every flagged K the warp stages the two tiles' norms
+//      of levels d-2, d-1, d in shared memory, and each lane runs the three
+//      remaining tests for its two output blocks, k ascending (k2, k1, k0
+//      loops); survivors per output block -> counts;
+//   3. an exclusive scan of the 4^d counts; 4. tl_tile<write>: the same walk
+//      writes each block's keys (Morton(i,j) << d | k) and (A slot, B slot)
+//      pairs at its offset -- already in the order the top-down expansion + a
+//      64-bit radix sort of all survivors produced (cfg2: 9.2e7 keys, 6.2 ms of
+//      expansion, sort, head flags and slot lookups per step -> see DESIGN).
+// The decisions are the same keep_pair tests on the same norms, so the set is
+// the expansion's bit for bit (tests: every survivor-set parity case, and the
+// old path stays behind SPG_TASKLIST=lists and for depth < 3 or > 12).
+constexpr int kTlWarps = 8;
+
+template <KeepRule R>
+__global__ void tl_valid(int s, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
+                         double tau, uint32_t row_lo, uint32_t row_hi,
+                         uint8_t* __restrict__ valid) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= (int64_t(1) << (3 * s))) return;
+  const uint64_t T = static_cast<uint64_t>(x) >> s;
+  const uint32_t K = static_cast<uint32_t>(x) & ((1u << s) - 1u);
+  const uint32_t I = morton_row(T), J = morton_col(T);
+  constexpr int kMaxS = 10;
+  double na[kMaxS], nb[kMaxS];
+#pragma unroll
+  for (int l = 0; l < kMaxS; ++l) {
+    if (l > s) break;
+    const int sh = s - l;
+    const int64_t off = level_offset(l);
+    na[l] = pyrA[off + morton2(I >> sh, K >> sh)];
+    nb[l] = pyrB[off + morton2(K >> sh, J >> sh)];
+  }
+  bool ok = I >= row_lo && I < row_hi;
+#pragma unroll
+  for (int l = 0; l < kMaxS; ++l) {
+    if (l > s) break;
+    ok = keep_pair<R>(na[l], nb[l], tau) && ok;
+  }
+  valid[x] = ok;
+}
+
+// WRITE = false: counts[T * 64 + m] = survivors of output block m of tile T.
+// WRITE = true: keys / pairs (each optional) at offsets[T * 64 + m] + rank.
+template <KeepRule R, bool WRITE>
+__global__ void __launch_bounds__(kTlWarps * 32)
+    tl_tile(int s, int d, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
+            double tau, const uint8_t* __restrict__ valid, int64_t* __restrict__ counts,
+            const int64_t* __restrict__ offsets, uint64_t* __restrict__ keys,
+            const int32_t* __restrict__ gridA, const int32_t* __restrict__ gridB,
+            int2* __restrict__ pairs, int* __restrict__ missing) {
+  __shared__ double sm[kTlWarps][2][84];  // per warp: A then B; levels d-2 (4), d-1 (16), d (64)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t T = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  if (T >= (int64_t(1) << (2 * s))) return;
+  const uint32_t I = morton_row(static_cast<uint64_t>(T)), J = morton_col(static_cast<uint64_t>(T));
+  const double* A2 = pyrA + level_offset(d - 2);
+  const double* A1 = pyrA + level_offset(d - 1);
+  const double* A0 = pyrA + level_offset(d);
+  const double* B2 = pyrB + level_offset(d - 2);
+  const double* B1 = pyrB + level_offset(d - 1);
+  const double* B0 = pyrB + level_offset(d);
+  double* sa = sm[warp][0];
+  double* sb = sm[warp][1];
+  // the lane's two output blocks m = lane, lane + 32 of the tile (local Morton
+  // index, digits 2 i_l + j_l from the top level down)
+  uint32_t i2[2], j2[2], i1[2], j1[2], i0[2], j0[2];
+  int64_t at[2];
+  int cnt[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t m = lane + 32 * h;
+    i2[h] = (m >> 5) & 1u; j2[h] = (m >> 4) & 1u;
+    i1[h] = (m >> 3) & 1u; j1[h] = (m >> 2) & 1u;
+    i0[h] = (m >> 1) & 1u; j0[h] = m & 1u;
+    at[h] = WRITE ? offsets[T * 64 + m] : 0;
+  }
+  const int n_k = 1 << s;
+  for (int Kb = 0; Kb < n_k; Kb += 32) {
+    const bool flag = Kb + lane < n_k && valid[(T << s) + Kb + lane] != 0;
+    uint32_t todo = __ballot_sync(0xffffffffu, flag);
+    while (todo) {
+      const uint32_t K = Kb + __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const int64_t mA = static_cast<int64_t>(morton2(I, K)), mB = static_cast<int64_t>(morton2(K, J));
+      __syncwarp();
+      sa[20 + lane] = A0[mA * 64 + lane];
+      sa[20 + 32 + lane] = A0[mA * 64 + 32 + lane];
+      sb[20 + lane] = B0[mB * 64 + lane];
+      sb[20 + 32 + lane] = B0[mB * 64 + 32 + lane];
+      if (lane < 16) {
+        sa[4 + lane] = A1[mA * 16 + lane];
+        sb[4 + lane] = B1[mB * 16 + lane];
+      } else if (lane < 20) {
+        sa[lane - 16] = A2[mA * 4 + lane - 16];
+        sb[lane - 16] = B2[mB * 4 + lane - 16];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (uint32_t k2 = 0; k2 < 2; ++k2) {
+          const uint32_t a2 = 2 * i2[h] + k2, b2 = 2 * k2 + j2[h];
+          if (!keep_pair<R>(sa[a2], sb[b2], tau)) continue;
+#pragma unroll
+          for (uint32_t k1 = 0; k1 < 2; ++k1) {
+            const uint32_t a1 = 4 * a2 + 2 * i1[h] + k1, b1 = 4 * b2 + 2 * k1 + j1[h];
+            if (!keep_pair<R>(sa[4 + a1], sb[4 + b1], tau)) continue;
+#pragma unroll
+            for (uint32_t k0 = 0; k0 < 2; ++k0) {
+              const uint32_t a0 = 4 * a1 + 2 * i0[h] + k0, b0 = 4 * b1 + 2 * k0 + j0[h];
+              if (!keep_pair<R>(sa[20 + a0], sb[20 + b0], tau)) continue;
+              if (WRITE) {
+                const int64_t pos = at[h] + cnt[h];
+                if (keys) {
+                  const uint64_t blk = static_cast<uint64_t>(T) * 64 + lane + 32 * h;
+                  keys[pos] = (blk << d) | (8 * K + 4 * k2 + 2 * k1 + k0);
+                }
+                if (pairs) {
+                  const int2 pr = make_int2(gridA[mA * 64 + a0], gridB[mB * 64 + b0]);
+                  pairs[pos] = pr;
+                  if (missing && (pr.x < 0 || pr.y < 0)) *missing = 1;
+                }
+              }
+              ++cnt[h];
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!WRITE) {
+    counts[T * 64 + lane] = cnt[0];
+    counts[T * 64 + 32 + lane] = cnt[1];
+  }
+}
+
+__global__ void tl_outputs(const int64_t* __restrict__ blocks, const int64_t* __restrict__ offsets,
+                           int64_t n_out, int64_t n_surv, uint64_t* __restrict__ out_keys,
+                           int64_t* __restrict__ out_offset) {
+  const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o > n_out) return;
+  if (o == n_out) {
+    out_offset[o] = n_surv;
+    return;
+  }
+  out_keys[o] = static_cast<uint64_t>(blocks[o]);
+  out_offset[o] = offsets[blocks[o]];
+}
+
+// developer switch SPG_TASKLIST=lists: the top-down expansion + radix sort
+bool dense_tasklist_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("SPG_TASKLIST");
+    return !(e && std::strcmp(e, "lists") == 0);
+  }();
+  return on;
+}
+
+struct DenseTasks {
+  int64_t n_surv = 0, n_out = 0;
+  DevBuf<uint64_t> keys, out_keys;
+  DevBuf<int64_t> out_offset;
+  DevBuf<int2> pairs;
+};
+
+// The dense path applies to trees of depth 3 .. 12 and shards of whole tile
+// rows; false = use the expansion.  want_keys / want_pairs choose the outputs
+// (pairs with their per-block ranges out_keys / out_offset).
+template <KeepRule R>
+bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
+                    Shard sh, bool want_keys, bool want_pairs, const spg_matrix* a_slots,
+                    DenseTasks* out) {
+  const int d = a->depth, s = d - 3;
+  if (!dense_tasklist_enabled() || s < 0 || s > 9 || sh.level > s) return false;
+  PhaseTrace tr(ctx, "tasklist.dense");
+  const uint32_t tile_rows = (1u << s) >> sh.level;
+  const uint32_t row_lo = tile_rows * static_cast<uint32_t>(sh.index), row_hi = row_lo + tile_rows;
+  const int64_t n_flags = int64_t(1) << (3 * s), n_tiles = int64_t(1) << (2 * s);
+  const int64_t n_blocks = n_tiles * 64;
+  DevBuf<uint8_t> valid(n_flags, ctx);
+  tl_valid<R><<<grid_for(n_flags, 256), 256, 0, ctx->stream>>>(s, a->pyramid, b->pyramid, tau,
+                                                               row_lo, row_hi, valid.get());
+  SPG_CHECK_LAUNCH(ctx);
+  DevBuf<int64_t> counts(n_blocks + 1, ctx), offsets(n_blocks + 1, ctx);
+  SPG_CUDA(cudaMemsetAsync(counts.get() + n_blocks, 0, sizeof(int64_t), ctx->stream));
+  const unsigned grid = static_cast<unsigned>((n_tiles + kTlWarps - 1) / kTlWarps);
+  tl_tile<R, false><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
+      s, d, a->pyramid, b->pyramid, tau, valid.get(), counts.get(), nullptr, nullptr, nullptr,
+      nullptr, nullptr, nullptr);
+  SPG_CHECK_LAUNCH(ctx);
+  out->n_surv = scan_counts(ctx, counts.get(), n_blocks, offsets.get());
+  out->n_out = 0;
+  if (out->n_surv == 0) return true;
+  if (want_keys) out->keys = DevBuf<uint64_t>(out->n_surv, ctx);
+  const bool split = want_pairs && a_slots != a;
+  DevBuf<int> missing(split ? 1 : 0, ctx);
+  if (split) SPG_CUDA(cudaMemsetAsync(missing.get(), 0, sizeof(int), ctx->stream));
+  if (want_pairs) out->pairs = DevBuf<int2>(out->n_surv, ctx);
+  tl_tile<R, true><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
+      s, d, a->pyramid, b->pyramid, tau, valid.get(), nullptr, offsets.get(),
+      want_keys ? out->keys.get() : nullptr, want_pairs ? a_slots->grid_slot : nullptr,
+      want_pairs ? b->grid_slot : nullptr, want_pairs ? out->pairs.get() : nullptr,
+      split ? missing.get() : nullptr);
+  SPG_CHECK_LAUNCH(ctx);
+  if (want_pairs) {
+    // the non-empty output blocks, ascending, with their pair ranges
+    DevBuf<int64_t> blocks(n_blocks, ctx), n_sel(1, ctx);
+    thrust::counting_iterator<int64_t> it(0);
+    size_t bytes = 0;
+    SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, counts.get(), blocks.get(),
+                                        n_sel.get(), n_blocks, ctx->stream));
+    DevBuf<uint8_t> tmp(bytes, ctx);
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, counts.get(), blocks.get(),
+                                        n_sel.get(), n_blocks, ctx->stream));
+    ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
+    out->n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
+    out->out_keys = DevBuf<uint64_t>(out->n_out, ctx);
+    out->out_offset = DevBuf<int64_t>(out->n_out + 1, ctx);
+    tl_outputs<<<grid_for(out->n_out + 1, 256), 256, 0, ctx->stream>>>(
+        blocks.get(), offsets.get(), out->n_out, out->n_surv, out->out_keys.get(),
+        out->out_offset.get());
+    SPG_CHECK_LAUNCH(ctx);
+    if (split) {
+      int h = 0;
+      SPG_CUDA(cudaMemcpyAsync(&h, missing.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h)
+        fail(SPG_EINVAL, "plan: a_norms lists a leaf in the shard rows that the local A does "
+                         "not hold (the shard rows of a and a_norms must have the same leaves)");
+    }
+  }
+  return true;
+}
+
 // Surviving (i,k,j) leaf products, sorted by (Morton(i,j), k); with a shard,
 // only the leaf products of its block-rows (ancestors above the shard level
 // are tested on the host, shard_list).
@@ -142,6 +387,14 @@ TaskList build_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix*
   TaskList tl;
   tl.kbits = d;
   PhaseTrace tr_all(ctx, "tasklist.total");
+  {
+    DenseTasks dt;
+    if (dense_tasklist<R>(ctx, a, b, tau, sh, true, false, nullptr, &dt)) {
+      tl.n_surv = dt.n_surv;
+      tl.keys = dt.n_surv ? std::move(dt.keys) : DevBuf<uint64_t>(1, ctx);
+      return tl;
+    }
+  }
   TripleList cur = sh.level == 0 ? root_list<R>(ctx, a, b, tau)
                                  : shard_list<R>(ctx, a, b, sh.level, sh.index, tau, true);
   DevBuf<uint64_t> keys;
@@ -413,6 +666,25 @@ Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, do
                   bool skip_test, Shard shard, bool keep_keys,
                   const spg_matrix* a_slots = nullptr) {
   if (!a_slots) a_slots = a;  // a: norms for the skip tests; a_slots: A's payload slots
+  {
+    DenseTasks dt;
+    const bool dense =
+        skip_test ? dense_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard, keep_keys, true,
+                                                    a_slots, &dt)
+                  : dense_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard, keep_keys, true,
+                                                     a_slots, &dt);
+    if (dense) {
+      Plan pl;
+      pl.n_surv = dt.n_surv;
+      pl.n_out = dt.n_out;
+      pl.kbits = a->depth;
+      pl.keys = std::move(dt.keys);
+      pl.out_keys = std::move(dt.out_keys);
+      pl.out_offset = std::move(dt.out_offset);
+      pl.pairs = std::move(dt.pairs);
+      return pl;
+    }
+  }
   TaskList tl = skip_test ? build_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard)
                           : build_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard);
   Plan pl;
