@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(kTlWarps * 32)
             const int32_t* __restrict__ gridA, const int32_t* __restrict__ gridB,
             int2* __restrict__ pairs, int* __restrict__ missing) {
   __shared__ double sm[kTlWarps][2][84];  // per warp: A then B; levels d-2 (4), d-1 (16), d (64)
+  __shared__ int64_t sm_at[kTlWarps][64];  // WRITE: next position of each output block
+  __shared__ uint8_t sm_mask[kTlWarps][64];  // WRITE: surviving k (3 bits) of each block at this K
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t T = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
   if (T >= (int64_t(1) << (2 * s))) return;
@@ -239,8 +241,10 @@ __global__ void __launch_bounds__(kTlWarps * 32)
         sb[lane - 16] = B2[mB * 4 + lane - 16];
       }
       __syncwarp();
+      // the surviving k of the lane's blocks at this K: bit 4 k2 + 2 k1 + k0
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
+        uint32_t mask = 0;
 #pragma unroll
         for (uint32_t k2 = 0; k2 < 2; ++k2) {
           const uint32_t a2 = 2 * i2[h] + k2, b2 = 2 * k2 + j2[h];
@@ -252,21 +256,37 @@ __global__ void __launch_bounds__(kTlWarps * 32)
 #pragma unroll
             for (uint32_t k0 = 0; k0 < 2; ++k0) {
               const uint32_t a0 = 4 * a1 + 2 * i0[h] + k0, b0 = 4 * b1 + 2 * k0 + j0[h];
-              if (!keep_pair<R>(sa[20 + a0], sb[20 + b0], tau)) continue;
-              if (WRITE) {
-                const int64_t pos = at[h] + cnt[h];
-                if (keys) {
-                  const uint64_t blk = static_cast<uint64_t>(T) * 64 + lane + 32 * h;
-                  keys[pos] = (blk << d) | (8 * K + 4 * k2 + 2 * k1 + k0);
-                }
-                if (pairs) {
-                  const int2 pr = make_int2(gridA[mA * 64 + a0], gridB[mB * 64 + b0]);
-                  pairs[pos] = pr;
-                  if (missing && (pr.x < 0 || pr.y < 0)) *missing = 1;
-                }
-              }
-              ++cnt[h];
+              if (keep_pair<R>(sa[20 + a0], sb[20 + b0], tau)) mask |= 1u << (4 * k2 + 2 * k1 + k0);
             }
+          }
+        }
+        if (WRITE) {
+          sm_mask[warp][lane + 32 * h] = static_cast<uint8_t>(mask);
+          sm_at[warp][lane + 32 * h] = at[h] + cnt[h];
+        }
+        cnt[h] += __popc(mask);
+      }
+      if (WRITE) {
+        // 8 lanes per output block (lane & 7 = the k bits), 4 blocks a round:
+        // a block's survivors go out as one contiguous run
+        __syncwarp();
+        const uint32_t kb = lane & 7u, k2 = kb >> 2, k1 = (kb >> 1) & 1u, k0 = kb & 1u;
+#pragma unroll 4
+        for (uint32_t r = 0; r < 16; ++r) {
+          const uint32_t blk = 4 * r + (lane >> 3);
+          const uint32_t mask = sm_mask[warp][blk];
+          if (!((mask >> kb) & 1u)) continue;
+          const int64_t pos = sm_at[warp][blk] + __popc(mask & ((1u << kb) - 1u));
+          if (keys)
+            keys[pos] = ((static_cast<uint64_t>(T) * 64 + blk) << d) | (8 * K + kb);
+          if (pairs) {
+            const uint32_t bi2 = (blk >> 5) & 1u, bj2 = (blk >> 4) & 1u, bi1 = (blk >> 3) & 1u,
+                           bj1 = (blk >> 2) & 1u, bi0 = (blk >> 1) & 1u, bj0 = blk & 1u;
+            const uint32_t a0 = 16 * (2 * bi2 + k2) + 4 * (2 * bi1 + k1) + 2 * bi0 + k0;
+            const uint32_t b0 = 16 * (2 * k2 + bj2) + 4 * (2 * k1 + bj1) + 2 * k0 + bj0;
+            const int2 pr = make_int2(gridA[mA * 64 + a0], gridB[mB * 64 + b0]);
+            pairs[pos] = pr;
+            if (missing && (pr.x < 0 || pr.y < 0)) *missing = 1;
           }
         }
       }
