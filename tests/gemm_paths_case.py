@@ -22,7 +22,8 @@ def digest(C):
 if __name__ == "__main__":
     ctx = nat.Context(0)
     for n, L, tau in [(4096, 32, 1e-9), (4096, 32, 0.0), (2080, 32, 1e-7),
-                      (8192, 128, 1e-9), (4224, 128, 0.0)]:
+                      (8192, 128, 1e-9), (4224, 128, 0.0), (4096, 64, 1e-8), (1000, 8, 1e-6),
+                      (40, 8, 1e-6)]:
         A = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 11, 1e-10)
         B = nat.synth_cluster_device(ctx, n, L, 3.0, 0.1, 2005, 12, 1e-10)
         C, st = nat.spamm(ctx, A, B, tau)

@@ -268,13 +268,15 @@ def test_sweep_paths_in_subprocesses(port, env):
         assert got[name] == want, (env, name)
 
 
-@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_SUPER32_QUAD": "0"}, {"SPG_GEMM128": "3"}])
+@pytest.mark.parametrize("env", [{"SPG_GEMM32": "6"}, {"SPG_SUPER32_QUAD": "0"}, {"SPG_GEMM128": "3"},
+                                 {"SPG_TASKLIST": "lists"}])
 def test_gemm_paths_in_subprocesses(env):
     """Leaf-GEMM variants that keep every block's products in ascending k and
     the same DMMA k-steps give C~ bit for bit equal to each other: the L = 32
     super-block kernel (default) against per-block tilings, L = 128 leaves as
-    L = 64 sub-products against the L = 128 kernel; the variant is fixed per
-    process."""
+    L = 64 sub-products against the L = 128 kernel; likewise the two task-list
+    builders (sort-free dense walk, default, against expansion + radix sort:
+    same survivors in the same order); the variant is fixed per process."""
     import os
     import subprocess
     import sys as _sys
