@@ -139,8 +139,8 @@ __global__ void triples_to_keys(const int32_t* __restrict__ I, const int32_t* __
 // in order: a product (i, k, j) survives iff every ancestor pair of it passes
 // the rule (multiply.cpp:70-76: spamm_node returns at the first null or
 // skipped pair), so
-//   1. tl_valid: one flag per (T, K), the pair (I, K, J) and its ancestors of
-//      levels 0 .. s pass (and I lies in the shard's rows);
+//   1. tl_valid: one flag per (T, K) of the shard's tile rows, the pair
+//      (I, K, J) and its ancestors of levels 0 .. s pass;
 //   2. tl_tile<count>: for every flagged K the warp stages the two tiles' norms
 //      of levels d-2, d-1, d in shared memory, and each lane runs the three
 //      remaining tests for its two output blocks, k ascending (k2, k1, k0
@@ -159,11 +159,12 @@ template <KeepRule R>
 __global__ void tl_valid(int s, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
                          double tau, uint32_t row_lo, uint32_t row_hi,
                          uint8_t* __restrict__ valid) {
+  // x = ((I - row_lo) * 2^s + J) * 2^s + K over the shard's tile rows
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= (int64_t(1) << (3 * s))) return;
-  const uint64_t T = static_cast<uint64_t>(x) >> s;
+  if (x >= (static_cast<int64_t>(row_hi - row_lo) << (2 * s))) return;
   const uint32_t K = static_cast<uint32_t>(x) & ((1u << s) - 1u);
-  const uint32_t I = morton_row(T), J = morton_col(T);
+  const uint32_t J = static_cast<uint32_t>(x >> s) & ((1u << s) - 1u);
+  const uint32_t I = row_lo + static_cast<uint32_t>(x >> (2 * s));
   constexpr int kMaxS = 10;
   double na[kMaxS], nb[kMaxS];
 #pragma unroll
@@ -174,7 +175,7 @@ __global__ void tl_valid(int s, const double* __restrict__ pyrA, const double* _
     na[l] = pyrA[off + morton2(I >> sh, K >> sh)];
     nb[l] = pyrB[off + morton2(K >> sh, J >> sh)];
   }
-  bool ok = I >= row_lo && I < row_hi;
+  bool ok = true;
 #pragma unroll
   for (int l = 0; l < kMaxS; ++l) {
     if (l > s) break;
@@ -188,7 +189,7 @@ __global__ void tl_valid(int s, const double* __restrict__ pyrA, const double* _
 template <KeepRule R, bool WRITE>
 __global__ void __launch_bounds__(kTlWarps * 32)
     tl_tile(int s, int d, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
-            double tau, const uint8_t* __restrict__ valid, int64_t* __restrict__ counts,
+            double tau, uint32_t row_lo, uint32_t row_hi, const uint8_t* __restrict__ valid, int64_t* __restrict__ counts,
             const int64_t* __restrict__ offsets, uint64_t* __restrict__ keys,
             const int32_t* __restrict__ gridA, const int32_t* __restrict__ gridB,
             int2* __restrict__ pairs, int* __restrict__ missing) {
@@ -196,9 +197,12 @@ __global__ void __launch_bounds__(kTlWarps * 32)
   __shared__ int64_t sm_at[kTlWarps][64];  // WRITE: next position of each output block
   __shared__ uint8_t sm_mask[kTlWarps][64];  // WRITE: surviving k (3 bits) of each block at this K
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t T = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
-  if (T >= (int64_t(1) << (2 * s))) return;
-  const uint32_t I = morton_row(static_cast<uint64_t>(T)), J = morton_col(static_cast<uint64_t>(T));
+  // the shard's tiles in (tile row, J) order; T = the tile's Morton index
+  const int64_t Tl = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  if (Tl >= (static_cast<int64_t>(row_hi - row_lo) << s)) return;
+  const uint32_t I = row_lo + static_cast<uint32_t>(Tl >> s);
+  const uint32_t J = static_cast<uint32_t>(Tl) & ((1u << s) - 1u);
+  const int64_t T = static_cast<int64_t>(morton2(I, J));
   const double* A2 = pyrA + level_offset(d - 2);
   const double* A1 = pyrA + level_offset(d - 1);
   const double* A0 = pyrA + level_offset(d);
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kTlWarps * 32)
   }
   const int n_k = 1 << s;
   for (int Kb = 0; Kb < n_k; Kb += 32) {
-    const bool flag = Kb + lane < n_k && valid[(T << s) + Kb + lane] != 0;
+    const bool flag = Kb + lane < n_k && valid[(Tl << s) + Kb + lane] != 0;
     uint32_t todo = __ballot_sync(0xffffffffu, flag);
     while (todo) {
       const uint32_t K = Kb + __ffs(todo) - 1;
@@ -298,6 +302,133 @@ __global__ void __launch_bounds__(kTlWarps * 32)
   }
 }
 
+// The same walk for the L = 32 super-block GEMM (leaf_gemm_super32): one entry
+// per (2x2 super block, k) with the 4-bit mask of the sub blocks present and
+// the A slots of rows 2I', 2I'+1 / B slots of columns 2J', 2J'+1 at that k,
+// super blocks in Morton order, k ascending -- what re-keying and key-value
+// sorting the survivor list produced (build_super32).  A tile holds 4 x 4 super
+// blocks; the four sub blocks of super block q are the tile's blocks 4q .. 4q+3
+// (four adjacent lanes).  WRITE = false: sb_counts[T * 16 + q] = entries.
+template <KeepRule R, bool WRITE>
+__global__ void __launch_bounds__(kTlWarps * 32)
+    tl_super(int s, int d, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
+             double tau, uint32_t row_lo, uint32_t row_hi, const uint8_t* __restrict__ valid, int64_t* __restrict__ sb_counts,
+             const int64_t* __restrict__ sb_offsets, const int32_t* __restrict__ gridA,
+             const int32_t* __restrict__ gridB, SuperEntry* __restrict__ ent,
+             uint32_t* __restrict__ emask, uint32_t* __restrict__ ek, int* __restrict__ missing) {
+  __shared__ double sm[kTlWarps][2][84];
+  __shared__ int64_t sm_at[kTlWarps][16];
+  __shared__ __align__(4) uint8_t sm_mask[kTlWarps][64];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the shard's tiles in (tile row, J) order; T = the tile's Morton index
+  const int64_t Tl = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  if (Tl >= (static_cast<int64_t>(row_hi - row_lo) << s)) return;
+  const uint32_t I = row_lo + static_cast<uint32_t>(Tl >> s);
+  const uint32_t J = static_cast<uint32_t>(Tl) & ((1u << s) - 1u);
+  const int64_t T = static_cast<int64_t>(morton2(I, J));
+  const double* A2 = pyrA + level_offset(d - 2);
+  const double* A1 = pyrA + level_offset(d - 1);
+  const double* A0 = pyrA + level_offset(d);
+  const double* B2 = pyrB + level_offset(d - 2);
+  const double* B1 = pyrB + level_offset(d - 1);
+  const double* B0 = pyrB + level_offset(d);
+  double* sa = sm[warp][0];
+  double* sb = sm[warp][1];
+  uint32_t i2[2], j2[2], i1[2], j1[2], i0[2], j0[2];
+  int64_t at[2];  // lanes 4q: next entry of super blocks q = lane / 4 and 8 + lane / 4
+  int cnt[2] = {0, 0};
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t m = lane + 32 * h;
+    i2[h] = (m >> 5) & 1u; j2[h] = (m >> 4) & 1u;
+    i1[h] = (m >> 3) & 1u; j1[h] = (m >> 2) & 1u;
+    i0[h] = (m >> 1) & 1u; j0[h] = m & 1u;
+    at[h] = WRITE ? sb_offsets[T * 16 + (m >> 2)] : 0;
+  }
+  const int n_k = 1 << s;
+  for (int Kb = 0; Kb < n_k; Kb += 32) {
+    const bool flag = Kb + lane < n_k && valid[(Tl << s) + Kb + lane] != 0;
+    uint32_t todo = __ballot_sync(0xffffffffu, flag);
+    while (todo) {
+      const uint32_t K = Kb + __ffs(todo) - 1;
+      todo &= todo - 1u;
+      const int64_t mA = static_cast<int64_t>(morton2(I, K)), mB = static_cast<int64_t>(morton2(K, J));
+      __syncwarp();
+      sa[20 + lane] = A0[mA * 64 + lane];
+      sa[20 + 32 + lane] = A0[mA * 64 + 32 + lane];
+      sb[20 + lane] = B0[mB * 64 + lane];
+      sb[20 + 32 + lane] = B0[mB * 64 + 32 + lane];
+      if (lane < 16) {
+        sa[4 + lane] = A1[mA * 16 + lane];
+        sb[4 + lane] = B1[mB * 16 + lane];
+      } else if (lane < 20) {
+        sa[lane - 16] = A2[mA * 4 + lane - 16];
+        sb[lane - 16] = B2[mB * 4 + lane - 16];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t mask = 0;
+#pragma unroll
+        for (uint32_t k2 = 0; k2 < 2; ++k2) {
+          const uint32_t a2 = 2 * i2[h] + k2, b2 = 2 * k2 + j2[h];
+          if (!keep_pair<R>(sa[a2], sb[b2], tau)) continue;
+#pragma unroll
+          for (uint32_t k1 = 0; k1 < 2; ++k1) {
+            const uint32_t a1 = 4 * a2 + 2 * i1[h] + k1, b1 = 4 * b2 + 2 * k1 + j1[h];
+            if (!keep_pair<R>(sa[4 + a1], sb[4 + b1], tau)) continue;
+#pragma unroll
+            for (uint32_t k0 = 0; k0 < 2; ++k0) {
+              const uint32_t a0 = 4 * a1 + 2 * i0[h] + k0, b0 = 4 * b1 + 2 * k0 + j0[h];
+              if (keep_pair<R>(sa[20 + a0], sb[20 + b0], tau)) mask |= 1u << (4 * k2 + 2 * k1 + k0);
+            }
+          }
+        }
+        // k with any of the super block's four sub blocks present
+        uint32_t any = mask | __shfl_xor_sync(0xffffffffu, mask, 1);
+        any |= __shfl_xor_sync(0xffffffffu, any, 2);
+        if (WRITE) {
+          sm_mask[warp][lane + 32 * h] = static_cast<uint8_t>(mask);
+          if ((lane & 3) == 0) sm_at[warp][(lane >> 2) + 8 * h] = at[h] + cnt[h];
+        }
+        cnt[h] += __popc(any);
+      }
+      if (WRITE) {
+        // 8 lanes per super block (lane & 7 = the k bits), 4 super blocks a round
+        __syncwarp();
+        const uint32_t kb = lane & 7u, k2 = kb >> 2, k1 = (kb >> 1) & 1u, k0 = kb & 1u;
+#pragma unroll
+        for (uint32_t r = 0; r < 4; ++r) {
+          const uint32_t q = 4 * r + (lane >> 3);
+          const uint32_t m4 = *reinterpret_cast<const uint32_t*>(&sm_mask[warp][4 * q]);
+          const uint32_t em = ((m4 >> kb) & 1u) | (((m4 >> (8 + kb)) & 1u) << 1) |
+                              (((m4 >> (16 + kb)) & 1u) << 2) | (((m4 >> (24 + kb)) & 1u) << 3);
+          if (!em) continue;
+          const uint32_t any = (m4 | (m4 >> 8) | (m4 >> 16) | (m4 >> 24)) & 0xffu;
+          const int64_t pos = sm_at[warp][q] + __popc(any & ((1u << kb) - 1u));
+          // super block q = local Morton (i2 j2 i1 j1); sub block = 2 r + c
+          const uint32_t qi2 = (q >> 3) & 1u, qj2 = (q >> 2) & 1u, qi1 = (q >> 1) & 1u, qj1 = q & 1u;
+          const uint32_t arow = 16 * (2 * qi2 + k2) + 4 * (2 * qi1 + k1) + k0;  // + 2 r
+          const uint32_t bcol = 16 * (2 * k2 + qj2) + 4 * (2 * k1 + qj1) + 2 * k0;  // + c
+          SuperEntry e{0, 0, 0, 0};
+          if (em & 0x3u) e.a0 = gridA[mA * 64 + arow];
+          if (em & 0xcu) e.a1 = gridA[mA * 64 + arow + 2];
+          if (em & 0x5u) e.b0 = gridB[mB * 64 + bcol];
+          if (em & 0xau) e.b1 = gridB[mB * 64 + bcol + 1];
+          if (missing && (e.a0 < 0 || e.a1 < 0 || e.b0 < 0 || e.b1 < 0)) *missing = 1;
+          ent[pos] = e;
+          emask[pos] = em;
+          ek[pos] = 8 * K + kb;
+        }
+      }
+    }
+  }
+  if (!WRITE && (lane & 3) == 0) {
+    sb_counts[T * 16 + (lane >> 2)] = cnt[0];
+    sb_counts[T * 16 + 8 + (lane >> 2)] = cnt[1];
+  }
+}
+
 __global__ void tl_outputs(const int64_t* __restrict__ blocks, const int64_t* __restrict__ offsets,
                            int64_t n_out, int64_t n_surv, uint64_t* __restrict__ out_keys,
                            int64_t* __restrict__ out_offset) {
@@ -333,24 +464,30 @@ struct DenseTasks {
 template <KeepRule R>
 bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                     Shard sh, bool want_keys, bool want_pairs, const spg_matrix* a_slots,
-                    DenseTasks* out) {
+                    DenseTasks* out, bool want_blocks = false) {
+  want_blocks = want_blocks || want_pairs;
   const int d = a->depth, s = d - 3;
   if (!dense_tasklist_enabled() || s < 0 || s > 9 || sh.level > s) return false;
   PhaseTrace tr(ctx, "tasklist.dense");
   const uint32_t tile_rows = (1u << s) >> sh.level;
   const uint32_t row_lo = tile_rows * static_cast<uint32_t>(sh.index), row_hi = row_lo + tile_rows;
-  const int64_t n_flags = int64_t(1) << (3 * s), n_tiles = int64_t(1) << (2 * s);
-  const int64_t n_blocks = n_tiles * 64;
+  // flags and warps cover the shard's tile rows only; the per-block counts
+  // stay indexed by global Morton order (zero outside the shard)
+  const int64_t n_tiles = static_cast<int64_t>(tile_rows) << s, n_flags = n_tiles << s;
+  const int64_t n_blocks = int64_t(64) << (2 * s);
   DevBuf<uint8_t> valid(n_flags, ctx);
   tl_valid<R><<<grid_for(n_flags, 256), 256, 0, ctx->stream>>>(s, a->pyramid, b->pyramid, tau,
                                                                row_lo, row_hi, valid.get());
   SPG_CHECK_LAUNCH(ctx);
   DevBuf<int64_t> counts(n_blocks + 1, ctx), offsets(n_blocks + 1, ctx);
-  SPG_CUDA(cudaMemsetAsync(counts.get() + n_blocks, 0, sizeof(int64_t), ctx->stream));
+  if (sh.level > 0)
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, (n_blocks + 1) * sizeof(int64_t), ctx->stream));
+  else
+    SPG_CUDA(cudaMemsetAsync(counts.get() + n_blocks, 0, sizeof(int64_t), ctx->stream));
   const unsigned grid = static_cast<unsigned>((n_tiles + kTlWarps - 1) / kTlWarps);
   tl_tile<R, false><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
-      s, d, a->pyramid, b->pyramid, tau, valid.get(), counts.get(), nullptr, nullptr, nullptr,
-      nullptr, nullptr, nullptr);
+      s, d, a->pyramid, b->pyramid, tau, row_lo, row_hi, valid.get(), counts.get(), nullptr,
+      nullptr, nullptr, nullptr, nullptr, nullptr);
   SPG_CHECK_LAUNCH(ctx);
   out->n_surv = scan_counts(ctx, counts.get(), n_blocks, offsets.get());
   out->n_out = 0;
@@ -360,13 +497,15 @@ bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, 
   DevBuf<int> missing(split ? 1 : 0, ctx);
   if (split) SPG_CUDA(cudaMemsetAsync(missing.get(), 0, sizeof(int), ctx->stream));
   if (want_pairs) out->pairs = DevBuf<int2>(out->n_surv, ctx);
-  tl_tile<R, true><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
-      s, d, a->pyramid, b->pyramid, tau, valid.get(), nullptr, offsets.get(),
-      want_keys ? out->keys.get() : nullptr, want_pairs ? a_slots->grid_slot : nullptr,
-      want_pairs ? b->grid_slot : nullptr, want_pairs ? out->pairs.get() : nullptr,
-      split ? missing.get() : nullptr);
-  SPG_CHECK_LAUNCH(ctx);
-  if (want_pairs) {
+  if (want_keys || want_pairs) {
+    tl_tile<R, true><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
+        s, d, a->pyramid, b->pyramid, tau, row_lo, row_hi, valid.get(), nullptr, offsets.get(),
+        want_keys ? out->keys.get() : nullptr, want_pairs ? a_slots->grid_slot : nullptr,
+        want_pairs ? b->grid_slot : nullptr, want_pairs ? out->pairs.get() : nullptr,
+        split ? missing.get() : nullptr);
+    SPG_CHECK_LAUNCH(ctx);
+  }
+  if (want_blocks) {
     // the non-empty output blocks, ascending, with their pair ranges
     DevBuf<int64_t> blocks(n_blocks, ctx), n_sel(1, ctx);
     thrust::counting_iterator<int64_t> it(0);
@@ -680,24 +819,43 @@ struct Plan {
   DevBuf<uint64_t> keys, out_keys;
   DevBuf<int64_t> out_offset;
   DevBuf<int2> pairs;
+  // built by the dense walk for the L = 32 super-block GEMM: no keys or pairs,
+  // build_super32 repeats the walk per super block from this recipe
+  bool dense_super = false;
+  const spg_matrix *src_a = nullptr, *src_b = nullptr, *src_slots = nullptr;
+  double tau = 0.0;
+  bool skip_test = true;
+  Shard shard;
 };
 
+// keep_keys: the sorted survivor keys stay (B panels, super-block re-keying);
+// for_super: the product runs through leaf_gemm_super32 -- with the dense walk
+// only the output blocks are produced here (implies keep_keys otherwise)
 Plan plan_product(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
                   bool skip_test, Shard shard, bool keep_keys,
-                  const spg_matrix* a_slots = nullptr) {
+                  const spg_matrix* a_slots = nullptr, bool for_super = false) {
   if (!a_slots) a_slots = a;  // a: norms for the skip tests; a_slots: A's payload slots
+  keep_keys = keep_keys || for_super;
   {
     DenseTasks dt;
+    const bool wk = keep_keys && !for_super, wp = !for_super;
     const bool dense =
-        skip_test ? dense_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard, keep_keys, true,
-                                                    a_slots, &dt)
-                  : dense_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard, keep_keys, true,
-                                                     a_slots, &dt);
+        skip_test ? dense_tasklist<KeepRule::kSkip>(ctx, a, b, tau, shard, wk, wp, a_slots, &dt,
+                                                    true)
+                  : dense_tasklist<KeepRule::kExact>(ctx, a, b, tau, shard, wk, wp, a_slots, &dt,
+                                                     true);
     if (dense) {
       Plan pl;
       pl.n_surv = dt.n_surv;
       pl.n_out = dt.n_out;
       pl.kbits = a->depth;
+      pl.dense_super = for_super;
+      pl.src_a = a;
+      pl.src_b = b;
+      pl.src_slots = a_slots;
+      pl.tau = tau;
+      pl.skip_test = skip_test;
+      pl.shard = shard;
       pl.keys = std::move(dt.keys);
       pl.out_keys = std::move(dt.out_keys);
       pl.out_offset = std::move(dt.out_offset);
@@ -830,7 +988,89 @@ struct Super32 {
   DevBuf<int32_t> sb_out, order;
 };
 
+// build_super32 by the dense walk (tl_super): entries straight from the norm
+// pyramids, no survivor keys, no sort.
+template <KeepRule R>
+Super32 dense_super32(spg_context* ctx, const Plan& pl) {
+  Super32 sp;
+  const spg_matrix *a = pl.src_a, *b = pl.src_b;
+  const int d = a->depth, s = d - 3;
+  PhaseTrace tr(ctx, "tasklist.dense_super");
+  const uint32_t tile_rows = (1u << s) >> pl.shard.level;
+  const uint32_t row_lo = tile_rows * static_cast<uint32_t>(pl.shard.index);
+  const uint32_t row_hi = row_lo + tile_rows;
+  const int64_t n_tiles = static_cast<int64_t>(tile_rows) << s, n_flags = n_tiles << s;
+  const int64_t n_sup = int64_t(16) << (2 * s);
+  DevBuf<uint8_t> valid(n_flags, ctx);
+  tl_valid<R><<<grid_for(n_flags, 256), 256, 0, ctx->stream>>>(
+      s, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get());
+  SPG_CHECK_LAUNCH(ctx);
+  DevBuf<int64_t> counts(n_sup + 1, ctx), offsets(n_sup + 1, ctx);
+  if (pl.shard.level > 0)
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, (n_sup + 1) * sizeof(int64_t), ctx->stream));
+  else
+    SPG_CUDA(cudaMemsetAsync(counts.get() + n_sup, 0, sizeof(int64_t), ctx->stream));
+  const unsigned grid = static_cast<unsigned>((n_tiles + kTlWarps - 1) / kTlWarps);
+  tl_super<R, false><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
+      s, d, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get(), counts.get(), nullptr,
+      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+  SPG_CHECK_LAUNCH(ctx);
+  const int64_t n_ent = scan_counts(ctx, counts.get(), n_sup, offsets.get());
+  sp.n_ent = n_ent;
+  if (n_ent == 0) return sp;
+  sp.ent = DevBuf<SuperEntry>(n_ent, ctx);
+  sp.emask = DevBuf<uint32_t>(n_ent, ctx);
+  sp.ek = DevBuf<uint32_t>(n_ent, ctx);
+  const bool split = pl.src_slots != a;
+  DevBuf<int> missing(split ? 1 : 0, ctx);
+  if (split) SPG_CUDA(cudaMemsetAsync(missing.get(), 0, sizeof(int), ctx->stream));
+  tl_super<R, true><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
+      s, d, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get(), nullptr, offsets.get(),
+      pl.src_slots->grid_slot, b->grid_slot, sp.ent.get(), sp.emask.get(), sp.ek.get(),
+      split ? missing.get() : nullptr);
+  SPG_CHECK_LAUNCH(ctx);
+  // the non-empty super blocks, ascending (Morton), with their entry ranges
+  DevBuf<int64_t> sbl(n_sup, ctx), n_sel(1, ctx);
+  thrust::counting_iterator<int64_t> it(0);
+  size_t bytes = 0;
+  SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, counts.get(), sbl.get(), n_sel.get(),
+                                      n_sup, ctx->stream));
+  {
+    DevBuf<uint8_t> tmp(bytes, ctx);
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, counts.get(), sbl.get(),
+                                        n_sel.get(), n_sup, ctx->stream));
+  }
+  ctx->lib_calls += 2;  // CUB device-wide primitives (library kernels)
+  const int64_t n_sb = copy_scalar_to_host_i64(ctx, n_sel.get());
+  sp.n_sb = n_sb;
+  sp.sb_offset = DevBuf<int64_t>(n_sb + 1, ctx);
+  DevBuf<uint64_t> sb_keys(n_sb, ctx);
+  tl_outputs<<<grid_for(n_sb + 1, 256), 256, 0, ctx->stream>>>(
+      sbl.get(), offsets.get(), n_sb, n_ent, sb_keys.get(), sp.sb_offset.get());
+  SPG_CHECK_LAUNCH(ctx);
+  sp.sb_out = DevBuf<int32_t>(4 * n_sb, ctx);
+  SPG_CUDA(cudaMemsetAsync(sp.sb_out.get(), 0xff, 4 * n_sb * sizeof(int32_t), ctx->stream));
+  super_out<<<grid_for(pl.n_out, 256), 256, 0, ctx->stream>>>(pl.out_keys.get(), pl.n_out,
+                                                              sb_keys.get(), n_sb,
+                                                              sp.sb_out.get());
+  SPG_CHECK_LAUNCH(ctx);
+  sp.order = make_block_order(ctx, sb_keys.get(), n_sb, n_sb);
+  if (split) {
+    int h = 0;
+    SPG_CUDA(cudaMemcpyAsync(&h, missing.get(), sizeof(int), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    SPG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h)
+      fail(SPG_EINVAL, "plan: a_norms lists a leaf in the shard rows that the local A does "
+                       "not hold (the shard rows of a and a_norms must have the same leaves)");
+  }
+  return sp;
+}
+
 Super32 build_super32(spg_context* ctx, int depth, const Plan& pl) {
+  if (pl.dense_super)
+    return pl.skip_test ? dense_super32<KeepRule::kSkip>(ctx, pl)
+                        : dense_super32<KeepRule::kExact>(ctx, pl);
   Super32 sp;
   const int64_t n = pl.n_surv;
   if (n == 0) return sp;
@@ -1204,7 +1444,7 @@ spg_matrix* spamm_device_chunked(spg_context* ctx, const spg_matrix* a, const sp
   try {
     for (int q = 0; q < nch; ++q) {
       SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-      Plan pl = plan_product(ctx, a, b, tau, skip_test, sub(q), super32);
+      Plan pl = plan_product(ctx, a, b, tau, skip_test, sub(q), false, nullptr, super32);
       SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
       if (pl.n_out != n_out[q]) fail(SPG_EINTERNAL, "chunked product: chunk size changed");
       if (pl.n_out) {
@@ -1264,7 +1504,7 @@ spg_matrix* spamm_device(spg_context* ctx, const spg_matrix* a, const spg_matrix
     if (c > 0) return spamm_device_chunked(ctx, a, b, tau, skip_test, stats, shard, c, super32);
   }
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  Plan plan = plan_product(ctx, a, b, tau, skip_test, shard, super32);
+  Plan plan = plan_product(ctx, a, b, tau, skip_test, shard, false, nullptr, super32);
   const int64_t n_surv = plan.n_surv, n_out = plan.n_out;
   DevBuf<uint64_t>& out_keys = plan.out_keys;
   DevBuf<int64_t>& out_offset = plan.out_offset;
@@ -1409,7 +1649,8 @@ spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b
   SPG_CUDA(cudaEventCreate(&plan->t_last));
   const int64_t LL = static_cast<int64_t>(a->leaf) * a->leaf;
   SPG_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  plan->pl = plan_product(ctx, a_norms ? a_norms : a, b, tau, true, shard, true, a);
+  plan->pl = plan_product(ctx, a_norms ? a_norms : a, b, tau, true, shard, true, a,
+                          a->leaf == 32 && super32_enabled());
   SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
   const int64_t n_out = plan->pl.n_out;
   plan->c = DevBuf<double>(std::max<int64_t>(n_out * LL, 1), ctx);
