@@ -1359,14 +1359,15 @@ void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_mat
 
 // Row chunks of a product whose task list would not fit (include/spamm_gpu.h
 // spg_context_set_task_budget): 2^c sub-shards of `sh`, one task list at a
-// time.  ~40 B per candidate bounds the build's peak (triples, masks, keys
-// and their sorted copy, pairs).
-// Row-chunk bits for a product whose task list would not fit: peak device
-// bytes per candidate leaf product of a plan (keys, pairs, the radix sort's
-// double buffers and temp storage) -- about 40 B, and 96 B when the L = 32
-// super-block re-keying (its own sort of 64-bit keys and values) follows --
-// against half of the free memory (plus this context's cached blocks) left
-// after `reserve` bytes for the output, whose chunks accumulate.
+// time.  Peak device bytes per candidate leaf product of a plan, against half
+// of the free memory (plus this context's cached blocks) left after `reserve`
+// bytes for the output, whose chunks accumulate:
+//  * dense walk (depth 3 .. 12, chunks of whole tile rows): 16 B -- a key and
+//    a slot pair per survivor; 24 B for the L = 32 super-block entries (slots,
+//    mask and k per entry, at most one entry per survivor);
+//  * expansion + radix sort (other depths, or chunks thinner than a tile row):
+//    about 40 B (triples, masks, keys and their sorted copy, sort temp, pairs),
+//    96 B when the super-block re-keying (its own key-value sort) follows.
 int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard sh,
                int max_bits, bool super32, int64_t reserve) {
   if (max_bits <= 0) return 0;
@@ -1379,12 +1380,22 @@ int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard
     const int64_t avail = static_cast<int64_t>(fr + cached) - std::max<int64_t>(reserve, 0);
     budget = std::max<int64_t>(avail / 2, static_cast<int64_t>(fr / 8));
   }
-  const double per_cand = super32 ? 96.0 : 40.0;
-  const double need = per_cand * static_cast<double>(count_candidates(ctx, a, b, sh));
-  int c = 0;
-  while (c < max_bits && need / static_cast<double>(int64_t(1) << c) > static_cast<double>(budget))
-    ++c;
-  return c;
+  const double cand = static_cast<double>(count_candidates(ctx, a, b, sh));
+  auto bits_for = [&](double per_cand, int limit) {
+    int c = 0;
+    while (c < limit && per_cand * cand / static_cast<double>(int64_t(1) << c) >
+                            static_cast<double>(budget))
+      ++c;
+    return per_cand * cand / static_cast<double>(int64_t(1) << c) <= static_cast<double>(budget)
+               ? c : -1;
+  };
+  const int s = a->depth - 3;
+  if (dense_tasklist_enabled() && s >= 0 && s <= 9 && sh.level <= s) {
+    const int c = bits_for(super32 ? 24.0 : 16.0, std::min(max_bits, s - sh.level));
+    if (c >= 0) return c;
+  }
+  const int c = bits_for(super32 ? 96.0 : 40.0, max_bits);
+  return c >= 0 ? c : max_bits;
 }
 
 // upper bound of an output's payload bytes: the shard's block rows x all
