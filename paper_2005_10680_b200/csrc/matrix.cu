@@ -54,9 +54,12 @@ PhaseTrace::~PhaseTrace() {
 
 void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
   bytes = (bytes + 511) & ~size_t(511);
-  // best fit among cached blocks, wasting at most half of the block
+  // best fit among cached blocks, wasting at most half of a small block and
+  // an eighth of a large one (config-4-sized products run within a few GB of
+  // the device's capacity: 2x blocks of several GB each exhausted it)
   auto it = free_blocks.lower_bound(bytes);
-  if (it != free_blocks.end() && it->first <= 2 * bytes + (size_t(1) << 20)) {
+  const size_t slack = bytes < (size_t(256) << 20) ? bytes + (size_t(1) << 20) : bytes / 8;
+  if (it != free_blocks.end() && it->first <= bytes + slack) {
     void* p = it->second;
     live[p] = it->first;
     free_blocks.erase(it);

@@ -1389,13 +1389,22 @@ int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard
     return per_cand * cand / static_cast<double>(int64_t(1) << c) <= static_cast<double>(budget)
                ? c : -1;
   };
+  static const bool trace = [] {
+    const char* e = std::getenv("SPG_TRACE");
+    return e && e[0] == '1';
+  }();
   const int s = a->depth - 3;
-  if (dense_tasklist_enabled() && s >= 0 && s <= 9 && sh.level <= s) {
-    const int c = bits_for(super32 ? 24.0 : 16.0, std::min(max_bits, s - sh.level));
-    if (c >= 0) return c;
+  int c = -1;
+  if (dense_tasklist_enabled() && s >= 0 && s <= 9 && sh.level <= s)
+    c = bits_for(super32 ? 24.0 : 16.0, std::min(max_bits, s - sh.level));
+  if (c < 0) {
+    c = bits_for(super32 ? 96.0 : 40.0, max_bits);
+    if (c < 0) c = max_bits;
   }
-  const int c = bits_for(super32 ? 96.0 : 40.0, max_bits);
-  return c >= 0 ? c : max_bits;
+  if (trace)
+    std::fprintf(stderr, "[spg] row chunks 2^%d: %.3g candidates, budget %.3g B (reserve %.3g B)\n",
+                 c, cand, static_cast<double>(budget), static_cast<double>(reserve));
+  return c;
 }
 
 // upper bound of an output's payload bytes: the shard's block rows x all
@@ -1437,7 +1446,8 @@ spg_matrix* spamm_device_chunked(spg_context* ctx, const spg_matrix* a, const sp
   std::vector<int64_t> n_out(static_cast<size_t>(nch));
   int64_t total_out = 0;
   for (int q = 0; q < nch; ++q) {
-    const Plan pl = plan_product(ctx, a, b, tau, skip_test, sub(q), false);
+    // sizing only: with the dense walk, for_super stops after the count pass
+    const Plan pl = plan_product(ctx, a, b, tau, skip_test, sub(q), false, nullptr, true);
     n_out[q] = pl.n_out;
     total_out += pl.n_out;
   }
@@ -1597,6 +1607,7 @@ struct EventSet {
 // rows in ascending order, so each C element sees the same FP64 operation
 // sequence as the resident product and C is bitwise identical to it.
 struct spg_plan {
+  bool external_c = false;  // c is a slice of the caller's payload (not owned)
   spg_context* ctx = nullptr;
   const spg_matrix* a = nullptr;
   const spg_matrix* b = nullptr;  // norm-only, slots sorted by block row
@@ -1637,8 +1648,12 @@ namespace spg {
 // a_norms (optional): the norms of the whole A when `a` holds only the
 // shard's block rows (skip tests above the shard level need the global
 // ancestors); the shard's rows of a_norms must be a's.
+// external_c: the plan's output blocks live in the caller's payload (row
+// chunks of one product written in place, plan_finish_into) instead of a
+// buffer of its own
 spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
-                      Shard shard, const spg_matrix* a_norms = nullptr) {
+                      Shard shard, const spg_matrix* a_norms = nullptr,
+                      double* external_c = nullptr) {
   if (a->dimension != b->dimension || a->leaf != b->leaf)
     fail(SPG_EINVAL, "multiply: dimension or leaf size mismatch");
   if (a_norms && (a_norms->dimension != a->dimension || a_norms->leaf != a->leaf))
@@ -1664,7 +1679,9 @@ spg_plan* plan_create(spg_context* ctx, const spg_matrix* a, const spg_matrix* b
                           a->leaf == 32 && super32_enabled());
   SPG_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
   const int64_t n_out = plan->pl.n_out;
-  plan->c = DevBuf<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+  plan->c = external_c ? DevBuf<double>::adopt(external_c, std::max<int64_t>(n_out * LL, 1), ctx)
+                       : DevBuf<double>(std::max<int64_t>(n_out * LL, 1), ctx);
+  plan->external_c = external_c != nullptr;
   if (n_out) SPG_CUDA(cudaMemsetAsync(plan->c.get(), 0, n_out * LL * sizeof(double), ctx->stream));
   plan->beg = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
   plan->end = DevBuf<int64_t>(std::max<int64_t>(n_out, 1), ctx);
@@ -1780,7 +1797,7 @@ void plan_run_table(spg_plan* plan, const double* const* h_table, int64_t n_tabl
   SPG_CUDA(cudaStreamSynchronize(ctx->stream));  // the table buffer returns to the pool
 }
 
-spg_matrix* plan_finish(spg_plan* plan) {
+spg_matrix* plan_finish(spg_plan* plan, uint64_t* keys_out = nullptr) {
   spg_context* ctx = plan->ctx;
   const spg_matrix* a = plan->a;
   const int32_t nb_logical = (a->dimension + a->leaf - 1) / a->leaf;
@@ -1796,8 +1813,18 @@ spg_matrix* plan_finish(spg_plan* plan) {
   plan->pl.keys.reset();
   plan->beg.reset();
   plan->end.reset();
-  spg_matrix* c = matrix_from_morton_blocks(ctx, a->dimension, a->leaf, plan->pl.n_out,
-                                            plan->pl.out_keys.release(), plan->c.release());
+  spg_matrix* c = nullptr;
+  if (plan->external_c) {  // blocks already in place: hand their keys over
+    if (!keys_out) fail(SPG_EINTERNAL, "plan: external output without a key array");
+    if (plan->pl.n_out)
+      SPG_CUDA(cudaMemcpyAsync(keys_out, plan->pl.out_keys.get(),
+                               plan->pl.n_out * sizeof(uint64_t), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    plan->c.release();
+  } else {
+    c = matrix_from_morton_blocks(ctx, a->dimension, a->leaf, plan->pl.n_out,
+                                  plan->pl.out_keys.release(), plan->c.release());
+  }
   SPG_CUDA(cudaEventRecord(ctx->ev[5], ctx->stream));
   SPG_CUDA(cudaEventSynchronize(ctx->ev[5]));
   SPG_CUDA(cudaEventElapsedTime(&plan->stats.ms_finalize, ctx->ev[4], ctx->ev[5]));
@@ -1902,8 +1929,11 @@ spg_matrix* spamm_panels_device(spg_context* ctx, std::unique_lock<std::mutex>& 
   const spg_matrix* an = a_norms ? a_norms : a;
   // super blocks pair rows 2I, 2I+1: a chunk keeps >= 2 rows for them
   const bool super32 = a->leaf == 32 && super32_enabled();
+  // reserved before the task lists are sized: the output's bound and the two
+  // panel buffers allocated below
   const int c = chunk_bits(ctx, an, b, sh, a->depth - sh.level - (super32 ? 1 : 0), super32,
-                           output_bytes_bound(a, sh));
+                           output_bytes_bound(a, sh) +
+                               2 * std::max<int64_t>(cap * LL, 1) * int64_t(sizeof(double)));
   std::vector<spg_matrix*> parts;
   struct Parts {
     std::vector<spg_matrix*>& v;
@@ -1911,14 +1941,45 @@ spg_matrix* spamm_panels_device(spg_context* ctx, std::unique_lock<std::mutex>& 
       for (spg_matrix* m : v) matrix_destroy(m);
     }
   } guard{parts};
+  // Several row chunks: every chunk's blocks go straight into one payload
+  // (sized by a pass over the chunks' output counts), so the product never
+  // holds C twice -- a config-4 rank keeps 52 GB of A rows and 69 GB of C.
+  const int nch = 1 << c;
+  auto sub = [&](int q) { return Shard{sh.level + c, (sh.index << c) + q}; };
+  std::vector<int64_t> n_out_q(static_cast<size_t>(nch), 0);
+  int64_t total_out = 0;
+  double* c_payload = nullptr;
+  uint64_t* c_keys = nullptr;
+  struct InPlace {
+    spg_context* ctx;
+    double*& pay;
+    uint64_t*& keys;
+    ~InPlace() {
+      if (pay) dev_free(pay, ctx);
+      if (keys) dev_free(keys, ctx);
+    }
+  } in_place{ctx, c_payload, c_keys};
+  if (nch > 1) {
+    for (int q = 0; q < nch; ++q) {
+      // sizing only: with the dense walk, for_super stops after the count pass
+      const Plan pl = plan_product(ctx, an, b, tau, true, sub(q), false, a, true);
+      n_out_q[q] = pl.n_out;
+      total_out += pl.n_out;
+    }
+    c_payload = dev_alloc<double>(std::max<int64_t>(total_out * LL, 1), ctx);
+    c_keys = dev_alloc<uint64_t>(std::max<int64_t>(total_out, 1), ctx);
+  }
+  int64_t out_off = 0;
   spg_spamm_stats total{};
   DevBuf<double> buf[2] = {DevBuf<double>(std::max<int64_t>(cap * LL, 1), ctx),
                            DevBuf<double>(std::max<int64_t>(cap * LL, 1), ctx)};
   cudaStream_t fs[2] = {ctx->copy_stream, ctx->h2d_stream};
   EventSet ev;  // e[0..1]: buffer i filled; e[2..3]: buffer i free again
-  for (int q = 0; q < (1 << c); ++q) {
-    std::unique_ptr<spg_plan> plan(
-        plan_create(ctx, a, b, tau, Shard{sh.level + c, (sh.index << c) + q}, a_norms));
+  for (int q = 0; q < nch; ++q) {
+    std::unique_ptr<spg_plan> plan(plan_create(
+        ctx, a, b, tau, sub(q), a_norms, nch > 1 ? c_payload + out_off * LL : nullptr));
+    if (nch > 1 && plan->pl.n_out != n_out_q[q])
+      fail(SPG_EINTERNAL, "panels: chunk size changed");
     SPG_CUDA(cudaEventRecord(ev.e[2], ctx->stream));
     SPG_CUDA(cudaEventRecord(ev.e[3], ctx->stream));
     std::vector<size_t> live;
@@ -1951,7 +2012,12 @@ spg_matrix* spamm_panels_device(spg_context* ctx, std::unique_lock<std::mutex>& 
         plan_accumulate(plan.get(), panels[p].first, panels[p].second, nullptr);
       }
     }
-    parts.push_back(plan_finish(plan.get()));
+    if (nch > 1) {
+      plan_finish(plan.get(), c_keys + out_off);
+      out_off += n_out_q[q];
+    } else {
+      parts.push_back(plan_finish(plan.get()));
+    }
     const spg_spamm_stats& st = plan->stats;
     total.candidates += st.candidates;
     total.survivors += st.survivors;
@@ -1963,11 +2029,16 @@ spg_matrix* spamm_panels_device(spg_context* ctx, std::unique_lock<std::mutex>& 
   }
   SPG_CUDA(cudaStreamSynchronize(ctx->stream));
   spg_matrix* out = nullptr;
-  if (parts.size() == 1) {
+  if (nch == 1) {
     out = parts[0];
     parts.clear();
   } else {
-    out = concat_row_chunks(ctx, parts);
+    // chunk keys are not globally in Morton order: the matrix scatters them
+    double* pay = c_payload;
+    uint64_t* keys = c_keys;
+    c_payload = nullptr;  // owned by the matrix from here on
+    c_keys = nullptr;
+    out = matrix_from_morton_blocks(ctx, a->dimension, a->leaf, total_out, keys, pay);
   }
   if (stats) *stats = total;
   return out;

@@ -123,7 +123,13 @@ base["bound_at_smallest_tau"] = float(bounds[-1])
 def cfetch(r0, r1, dst, count, stream):
     # spg_spamm_panels' callback: the owner's broadcast on 8 GPUs; here the
     # panel is generated in place and its leaves gathered into dst on `stream`
-    Bp = nat.synth_cluster_device_rows_scaled(ctx, N, L, ELL, DENS, SITE, SEED_B, DROP, sB, r0, r1)
+    try:
+        Bp = nat.synth_cluster_device_rows_scaled(ctx, N, L, ELL, DENS, SITE, SEED_B, DROP, sB, r0, r1)
+    except MemoryError:
+        free, total = torch.cuda.mem_get_info()
+        print(f"[cfg4_shard] panel [{r0}, {r1}) generation out of memory: device free "
+              f"{free / 2**30:.1f} of {total / 2**30:.1f} GiB", file=sys.stderr, flush=True)
+        raise
     ctx.synchronize()
     nat.gather_rows(Bp, r0, r1, dst, count, stream)
     torch.cuda.ExternalStream(stream).synchronize()  # before Bp's memory is reused
