@@ -1274,7 +1274,12 @@ void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_mat
   DevBuf<double> norms(n_out, ctx);
   DevBuf<uint8_t> nz(n_out, ctx);
   const int32_t nb = (a->dimension + L - 1) / L;
-  const int64_t n_chunks = std::min<int64_t>(32, std::max<int64_t>(1, n_out / 4096));
+  // developer switch SPG_STREAM_CHUNKS: upper bound of the chunk count
+  static const int64_t max_chunks = [] {
+    const char* e = std::getenv("SPG_STREAM_CHUNKS");
+    return e && std::atoi(e) > 0 ? static_cast<int64_t>(std::atoi(e)) : int64_t(32);
+  }();
+  const int64_t n_chunks = std::min<int64_t>(max_chunks, std::max<int64_t>(1, n_out / 4096));
   const int64_t cs = (n_out + n_chunks - 1) / n_chunks;
   // row-major CTA order inside each chunk (indices local to the chunk)
   DevBuf<int32_t> order = make_block_order(ctx, out_keys.get(), n_out, cs);
