@@ -6,10 +6,13 @@
 // !(fl(nA*nB) < tau) is applied top-down at EVERY level (root included) on
 // the dense norm pyramids, so even the underflow corner where an inner norm is
 // below a child's (sqrt(fl(x*x)) < x for subnormal squares) skips exactly what
-// the reference skips.  The leaf level writes sort keys
-// (Morton(i,j) << depth) | k; a deterministic radix sort groups them by
-// output block in Morton order with k ascending; run heads give each output
-// block's [begin, end) range of (A slot, B slot) pairs for K5.
+// the reference skips.  K5 takes, per output block in Morton order, the
+// [begin, end) range of its (A slot, B slot) pairs with k ascending: for
+// trees of depth 3 .. 12 a dense walk per output tile produces them directly
+// in that order (below: tl_valid / tl_tile / tl_super); otherwise the tree is
+// expanded level by level, the leaf level writes sort keys
+// (Morton(i,j) << depth) | k, a deterministic radix sort groups them and run
+// heads give the ranges.
 //
 // C (multiply.cpp:16-20, quadtree.cpp:24-36): one leaf per output block with
 // >= 1 survivor; its norm follows block_norm (K1); all-zero sums collapse to
