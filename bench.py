@@ -491,6 +491,16 @@ def run_ours(args, dist):
                             "frac_of_spec_7700": round(norm_bytes / (norm_ms / 1e3) / 1e9 / 7700.0,
                                                        4),
                             "ms": round(norm_ms, 3), "algorithmic": "8 L^2 B read per leaf"}
+    # K4 (task list: skip tests of every level, survivors grouped by output
+    # block with k ascending): 8 B key + 8 B slot pair per survivor
+    tl_ms = out["phase_ms"]["tasklist"]
+    if tl_ms > 0:
+        tl_gbs = 16.0 * surv / (tl_ms / 1e3) / 1e9
+        out["tasklist_roofline"] = {"kernel": "tl_valid + tl_tile<count> + scan + tl_tile<write> (K4)",
+                                    "bound": "hbm", "achieved": round(tl_gbs, 1), "peak": hbm,
+                                    "unit": "GB/s", "frac": round(tl_gbs / hbm, 4),
+                                    "peak_source": hbm_src, "ms": tl_ms,
+                                    "algorithmic": "8 B key + 8 B pair per surviving leaf product"}
     if distributed:
         out["panel_bytes_per_step"] = int(st["panel_bytes"])
     if not split:  # SURVEY 8a parity audit: how close the decisions are to ties

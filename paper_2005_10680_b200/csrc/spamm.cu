@@ -191,8 +191,9 @@ __global__ void tl_valid(int s, const double* __restrict__ pyrA, const double* _
 // WRITE = true: keys / pairs (each optional) at offsets[T * 64 + m] + rank.
 template <KeepRule R, bool WRITE>
 __global__ void __launch_bounds__(kTlWarps * 32)
-    tl_tile(int s, int d, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
-            double tau, uint32_t row_lo, uint32_t row_hi, const uint8_t* __restrict__ valid, int64_t* __restrict__ counts,
+    tl_tile(int s, int d, int pl, const double* __restrict__ pyrA,
+            const double* __restrict__ pyrB, double tau, uint32_t row_lo, uint32_t row_hi,
+            const uint8_t* __restrict__ valid, int64_t* __restrict__ counts,
             const int64_t* __restrict__ offsets, uint64_t* __restrict__ keys,
             const int32_t* __restrict__ gridA, const int32_t* __restrict__ gridB,
             int2* __restrict__ pairs, int* __restrict__ missing) {
@@ -200,8 +201,12 @@ __global__ void __launch_bounds__(kTlWarps * 32)
   __shared__ int64_t sm_at[kTlWarps][64];  // WRITE: next position of each output block
   __shared__ uint8_t sm_mask[kTlWarps][64];  // WRITE: surviving k (3 bits) of each block at this K
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // the shard's tiles in (tile row, J) order; T = the tile's Morton index
-  const int64_t Tl = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  // the shard's tiles in (tile row, J) order, 2^pl warps per tile, each with
+  // its own stretch of K (small problems have too few tiles to fill the
+  // machine); T = the tile's Morton index
+  const int64_t W = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  const int64_t Tl = W >> pl;
+  const int part = static_cast<int>(W & ((int64_t(1) << pl) - 1));
   if (Tl >= (static_cast<int64_t>(row_hi - row_lo) << s)) return;
   const uint32_t I = row_lo + static_cast<uint32_t>(Tl >> s);
   const uint32_t J = static_cast<uint32_t>(Tl) & ((1u << s) - 1u);
@@ -225,11 +230,11 @@ __global__ void __launch_bounds__(kTlWarps * 32)
     i2[h] = (m >> 5) & 1u; j2[h] = (m >> 4) & 1u;
     i1[h] = (m >> 3) & 1u; j1[h] = (m >> 2) & 1u;
     i0[h] = (m >> 1) & 1u; j0[h] = m & 1u;
-    at[h] = WRITE ? offsets[T * 64 + m] : 0;
+    at[h] = WRITE ? offsets[((T * 64 + m) << pl) + part] : 0;
   }
-  const int n_k = 1 << s;
-  for (int Kb = 0; Kb < n_k; Kb += 32) {
-    const bool flag = Kb + lane < n_k && valid[(Tl << s) + Kb + lane] != 0;
+  const int k_len = (1 << s) >> pl, k_end = (part + 1) * k_len;
+  for (int Kb = part * k_len; Kb < k_end; Kb += 32) {
+    const bool flag = Kb + lane < k_end && valid[(Tl << s) + Kb + lane] != 0;
     uint32_t todo = __ballot_sync(0xffffffffu, flag);
     while (todo) {
       const uint32_t K = Kb + __ffs(todo) - 1;
@@ -300,8 +305,8 @@ __global__ void __launch_bounds__(kTlWarps * 32)
     }
   }
   if (!WRITE) {
-    counts[T * 64 + lane] = cnt[0];
-    counts[T * 64 + 32 + lane] = cnt[1];
+    counts[((T * 64 + lane) << pl) + part] = cnt[0];
+    counts[((T * 64 + 32 + lane) << pl) + part] = cnt[1];
   }
 }
 
@@ -314,8 +319,9 @@ __global__ void __launch_bounds__(kTlWarps * 32)
 // (four adjacent lanes).  WRITE = false: sb_counts[T * 16 + q] = entries.
 template <KeepRule R, bool WRITE>
 __global__ void __launch_bounds__(kTlWarps * 32)
-    tl_super(int s, int d, const double* __restrict__ pyrA, const double* __restrict__ pyrB,
-             double tau, uint32_t row_lo, uint32_t row_hi, const uint8_t* __restrict__ valid, int64_t* __restrict__ sb_counts,
+    tl_super(int s, int d, int pl, const double* __restrict__ pyrA,
+             const double* __restrict__ pyrB, double tau, uint32_t row_lo, uint32_t row_hi,
+             const uint8_t* __restrict__ valid, int64_t* __restrict__ sb_counts,
              const int64_t* __restrict__ sb_offsets, const int32_t* __restrict__ gridA,
              const int32_t* __restrict__ gridB, SuperEntry* __restrict__ ent,
              uint32_t* __restrict__ emask, uint32_t* __restrict__ ek, int* __restrict__ missing) {
@@ -323,8 +329,12 @@ __global__ void __launch_bounds__(kTlWarps * 32)
   __shared__ int64_t sm_at[kTlWarps][16];
   __shared__ __align__(4) uint8_t sm_mask[kTlWarps][64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // the shard's tiles in (tile row, J) order; T = the tile's Morton index
-  const int64_t Tl = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  // the shard's tiles in (tile row, J) order, 2^pl warps per tile, each with
+  // its own stretch of K (small problems have too few tiles to fill the
+  // machine); T = the tile's Morton index
+  const int64_t W = static_cast<int64_t>(blockIdx.x) * kTlWarps + warp;
+  const int64_t Tl = W >> pl;
+  const int part = static_cast<int>(W & ((int64_t(1) << pl) - 1));
   if (Tl >= (static_cast<int64_t>(row_hi - row_lo) << s)) return;
   const uint32_t I = row_lo + static_cast<uint32_t>(Tl >> s);
   const uint32_t J = static_cast<uint32_t>(Tl) & ((1u << s) - 1u);
@@ -346,11 +356,11 @@ __global__ void __launch_bounds__(kTlWarps * 32)
     i2[h] = (m >> 5) & 1u; j2[h] = (m >> 4) & 1u;
     i1[h] = (m >> 3) & 1u; j1[h] = (m >> 2) & 1u;
     i0[h] = (m >> 1) & 1u; j0[h] = m & 1u;
-    at[h] = WRITE ? sb_offsets[T * 16 + (m >> 2)] : 0;
+    at[h] = WRITE ? sb_offsets[((T * 16 + (m >> 2)) << pl) + part] : 0;
   }
-  const int n_k = 1 << s;
-  for (int Kb = 0; Kb < n_k; Kb += 32) {
-    const bool flag = Kb + lane < n_k && valid[(Tl << s) + Kb + lane] != 0;
+  const int k_len = (1 << s) >> pl, k_end = (part + 1) * k_len;
+  for (int Kb = part * k_len; Kb < k_end; Kb += 32) {
+    const bool flag = Kb + lane < k_end && valid[(Tl << s) + Kb + lane] != 0;
     uint32_t todo = __ballot_sync(0xffffffffu, flag);
     while (todo) {
       const uint32_t K = Kb + __ffs(todo) - 1;
@@ -427,13 +437,14 @@ __global__ void __launch_bounds__(kTlWarps * 32)
     }
   }
   if (!WRITE && (lane & 3) == 0) {
-    sb_counts[T * 16 + (lane >> 2)] = cnt[0];
-    sb_counts[T * 16 + 8 + (lane >> 2)] = cnt[1];
+    sb_counts[((T * 16 + (lane >> 2)) << pl) + part] = cnt[0];
+    sb_counts[((T * 16 + 8 + (lane >> 2)) << pl) + part] = cnt[1];
   }
 }
 
+// offsets hold 2^pl K-parts per block: a block's range starts at its first part
 __global__ void tl_outputs(const int64_t* __restrict__ blocks, const int64_t* __restrict__ offsets,
-                           int64_t n_out, int64_t n_surv, uint64_t* __restrict__ out_keys,
+                           int pl, int64_t n_out, int64_t n_surv, uint64_t* __restrict__ out_keys,
                            int64_t* __restrict__ out_offset) {
   const int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (o > n_out) return;
@@ -442,7 +453,22 @@ __global__ void tl_outputs(const int64_t* __restrict__ blocks, const int64_t* __
     return;
   }
   out_keys[o] = static_cast<uint64_t>(blocks[o]);
-  out_offset[o] = offsets[blocks[o]];
+  out_offset[o] = offsets[blocks[o] << pl];
+}
+
+// survivors per block over its 2^pl K-parts (the flags of the block select)
+__global__ void tl_block_totals(const int64_t* __restrict__ offsets, int64_t n_blocks, int pl,
+                                int64_t* __restrict__ totals) {
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (b < n_blocks) totals[b] = offsets[(b + 1) << pl] - offsets[b << pl];
+}
+
+// 2^pl warps per tile so that a small problem still fills the machine
+int tile_parts_log(const spg_context* ctx, int64_t n_tiles, int s) {
+  const int64_t want = static_cast<int64_t>(ctx->sm_count) * 64;
+  int pl = 0;
+  while (pl < s && (n_tiles << pl) < want) ++pl;
+  return pl;
 }
 
 // developer switch SPG_TASKLIST=lists: the top-down expansion + radix sort
@@ -482,17 +508,19 @@ bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, 
   tl_valid<R><<<grid_for(n_flags, 256), 256, 0, ctx->stream>>>(s, a->pyramid, b->pyramid, tau,
                                                                row_lo, row_hi, valid.get());
   SPG_CHECK_LAUNCH(ctx);
-  DevBuf<int64_t> counts(n_blocks + 1, ctx), offsets(n_blocks + 1, ctx);
+  const int pl = tile_parts_log(ctx, n_tiles, s);
+  const int64_t n_cnt = n_blocks << pl;
+  DevBuf<int64_t> counts(n_cnt + 1, ctx), offsets(n_cnt + 1, ctx);
   if (sh.level > 0)
-    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, (n_blocks + 1) * sizeof(int64_t), ctx->stream));
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, (n_cnt + 1) * sizeof(int64_t), ctx->stream));
   else
-    SPG_CUDA(cudaMemsetAsync(counts.get() + n_blocks, 0, sizeof(int64_t), ctx->stream));
-  const unsigned grid = static_cast<unsigned>((n_tiles + kTlWarps - 1) / kTlWarps);
+    SPG_CUDA(cudaMemsetAsync(counts.get() + n_cnt, 0, sizeof(int64_t), ctx->stream));
+  const unsigned grid = static_cast<unsigned>(((n_tiles << pl) + kTlWarps - 1) / kTlWarps);
   tl_tile<R, false><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
-      s, d, a->pyramid, b->pyramid, tau, row_lo, row_hi, valid.get(), counts.get(), nullptr,
+      s, d, pl, a->pyramid, b->pyramid, tau, row_lo, row_hi, valid.get(), counts.get(), nullptr,
       nullptr, nullptr, nullptr, nullptr, nullptr);
   SPG_CHECK_LAUNCH(ctx);
-  out->n_surv = scan_counts(ctx, counts.get(), n_blocks, offsets.get());
+  out->n_surv = scan_counts(ctx, counts.get(), n_cnt, offsets.get());
   out->n_out = 0;
   if (out->n_surv == 0) return true;
   if (want_keys) out->keys = DevBuf<uint64_t>(out->n_surv, ctx);
@@ -502,7 +530,8 @@ bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, 
   if (want_pairs) out->pairs = DevBuf<int2>(out->n_surv, ctx);
   if (want_keys || want_pairs) {
     tl_tile<R, true><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
-        s, d, a->pyramid, b->pyramid, tau, row_lo, row_hi, valid.get(), nullptr, offsets.get(),
+        s, d, pl, a->pyramid, b->pyramid, tau, row_lo, row_hi, valid.get(), nullptr,
+        offsets.get(),
         want_keys ? out->keys.get() : nullptr, want_pairs ? a_slots->grid_slot : nullptr,
         want_pairs ? b->grid_slot : nullptr, want_pairs ? out->pairs.get() : nullptr,
         split ? missing.get() : nullptr);
@@ -510,20 +539,27 @@ bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, 
   }
   if (want_blocks) {
     // the non-empty output blocks, ascending, with their pair ranges
-    DevBuf<int64_t> blocks(n_blocks, ctx), n_sel(1, ctx);
+    DevBuf<int64_t> blocks(n_blocks, ctx), n_sel(1, ctx), totals(pl ? n_blocks : 0, ctx);
+    const int64_t* per_block = counts.get();
+    if (pl) {
+      tl_block_totals<<<grid_for(n_blocks, 256), 256, 0, ctx->stream>>>(offsets.get(), n_blocks,
+                                                                        pl, totals.get());
+      SPG_CHECK_LAUNCH(ctx);
+      per_block = totals.get();
+    }
     thrust::counting_iterator<int64_t> it(0);
     size_t bytes = 0;
-    SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, counts.get(), blocks.get(),
+    SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, per_block, blocks.get(),
                                         n_sel.get(), n_blocks, ctx->stream));
     DevBuf<uint8_t> tmp(bytes, ctx);
-    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, counts.get(), blocks.get(),
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, per_block, blocks.get(),
                                         n_sel.get(), n_blocks, ctx->stream));
     ctx->lib_calls++;  // CUB device-wide primitive (library kernels)
     out->n_out = copy_scalar_to_host_i64(ctx, n_sel.get());
     out->out_keys = DevBuf<uint64_t>(out->n_out, ctx);
     out->out_offset = DevBuf<int64_t>(out->n_out + 1, ctx);
     tl_outputs<<<grid_for(out->n_out + 1, 256), 256, 0, ctx->stream>>>(
-        blocks.get(), offsets.get(), out->n_out, out->n_surv, out->out_keys.get(),
+        blocks.get(), offsets.get(), pl, out->n_out, out->n_surv, out->out_keys.get(),
         out->out_offset.get());
     SPG_CHECK_LAUNCH(ctx);
     if (split) {
@@ -1008,17 +1044,19 @@ Super32 dense_super32(spg_context* ctx, const Plan& pl) {
   tl_valid<R><<<grid_for(n_flags, 256), 256, 0, ctx->stream>>>(
       s, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get());
   SPG_CHECK_LAUNCH(ctx);
-  DevBuf<int64_t> counts(n_sup + 1, ctx), offsets(n_sup + 1, ctx);
+  const int kp = tile_parts_log(ctx, n_tiles, s);
+  const int64_t n_cnt = n_sup << kp;
+  DevBuf<int64_t> counts(n_cnt + 1, ctx), offsets(n_cnt + 1, ctx);
   if (pl.shard.level > 0)
-    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, (n_sup + 1) * sizeof(int64_t), ctx->stream));
+    SPG_CUDA(cudaMemsetAsync(counts.get(), 0, (n_cnt + 1) * sizeof(int64_t), ctx->stream));
   else
-    SPG_CUDA(cudaMemsetAsync(counts.get() + n_sup, 0, sizeof(int64_t), ctx->stream));
-  const unsigned grid = static_cast<unsigned>((n_tiles + kTlWarps - 1) / kTlWarps);
+    SPG_CUDA(cudaMemsetAsync(counts.get() + n_cnt, 0, sizeof(int64_t), ctx->stream));
+  const unsigned grid = static_cast<unsigned>(((n_tiles << kp) + kTlWarps - 1) / kTlWarps);
   tl_super<R, false><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
-      s, d, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get(), counts.get(), nullptr,
-      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
+      s, d, kp, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get(), counts.get(),
+      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   SPG_CHECK_LAUNCH(ctx);
-  const int64_t n_ent = scan_counts(ctx, counts.get(), n_sup, offsets.get());
+  const int64_t n_ent = scan_counts(ctx, counts.get(), n_cnt, offsets.get());
   sp.n_ent = n_ent;
   if (n_ent == 0) return sp;
   sp.ent = DevBuf<SuperEntry>(n_ent, ctx);
@@ -1028,20 +1066,28 @@ Super32 dense_super32(spg_context* ctx, const Plan& pl) {
   DevBuf<int> missing(split ? 1 : 0, ctx);
   if (split) SPG_CUDA(cudaMemsetAsync(missing.get(), 0, sizeof(int), ctx->stream));
   tl_super<R, true><<<grid, kTlWarps * 32, 0, ctx->stream>>>(
-      s, d, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get(), nullptr, offsets.get(),
+      s, d, kp, a->pyramid, b->pyramid, pl.tau, row_lo, row_hi, valid.get(), nullptr,
+      offsets.get(),
       pl.src_slots->grid_slot, b->grid_slot, sp.ent.get(), sp.emask.get(), sp.ek.get(),
       split ? missing.get() : nullptr);
   SPG_CHECK_LAUNCH(ctx);
   // the non-empty super blocks, ascending (Morton), with their entry ranges
-  DevBuf<int64_t> sbl(n_sup, ctx), n_sel(1, ctx);
+  DevBuf<int64_t> sbl(n_sup, ctx), n_sel(1, ctx), totals(kp ? n_sup : 0, ctx);
+  const int64_t* per_sb = counts.get();
+  if (kp) {
+    tl_block_totals<<<grid_for(n_sup, 256), 256, 0, ctx->stream>>>(offsets.get(), n_sup, kp,
+                                                                   totals.get());
+    SPG_CHECK_LAUNCH(ctx);
+    per_sb = totals.get();
+  }
   thrust::counting_iterator<int64_t> it(0);
   size_t bytes = 0;
-  SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, counts.get(), sbl.get(), n_sel.get(),
-                                      n_sup, ctx->stream));
+  SPG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, per_sb, sbl.get(), n_sel.get(), n_sup,
+                                      ctx->stream));
   {
     DevBuf<uint8_t> tmp(bytes, ctx);
-    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, counts.get(), sbl.get(),
-                                        n_sel.get(), n_sup, ctx->stream));
+    SPG_CUDA(cub::DeviceSelect::Flagged(tmp.get(), bytes, it, per_sb, sbl.get(), n_sel.get(),
+                                        n_sup, ctx->stream));
   }
   ctx->lib_calls += 2;  // CUB device-wide primitives (library kernels)
   const int64_t n_sb = copy_scalar_to_host_i64(ctx, n_sel.get());
@@ -1049,7 +1095,7 @@ Super32 dense_super32(spg_context* ctx, const Plan& pl) {
   sp.sb_offset = DevBuf<int64_t>(n_sb + 1, ctx);
   DevBuf<uint64_t> sb_keys(n_sb, ctx);
   tl_outputs<<<grid_for(n_sb + 1, 256), 256, 0, ctx->stream>>>(
-      sbl.get(), offsets.get(), n_sb, n_ent, sb_keys.get(), sp.sb_offset.get());
+      sbl.get(), offsets.get(), kp, n_sb, n_ent, sb_keys.get(), sp.sb_offset.get());
   SPG_CHECK_LAUNCH(ctx);
   sp.sb_out = DevBuf<int32_t>(4 * n_sb, ctx);
   SPG_CUDA(cudaMemsetAsync(sp.sb_out.get(), 0xff, 4 * n_sb * sizeof(int32_t), ctx->stream));
