@@ -52,8 +52,23 @@ PhaseTrace::~PhaseTrace() {
   }
 }
 
+// Block sizes between 1 MB and 16 GB are rounded up to eight classes per
+// octave (at most 12.5 % over the request): task-list buffers follow the
+// survivor count, which differs a little from product to product, and exact
+// sizes missed the cache -- a cudaMalloc (and, with the device nearly full, a
+// trim of the whole cache) between two kernels showed up as 200-500 ms
+// task-list times on single cells.  Larger blocks (operand and product
+// payloads of configs 4/5, within a few GB of the device's capacity) stay
+// exact.
+static size_t size_class(size_t bytes) {
+  if (bytes < (size_t(1) << 20) || bytes >= (size_t(16) << 30)) return bytes;
+  size_t step = size_t(1) << 17;  // octave / 8 for the first octave (1 MB)
+  while ((step << 4) <= bytes) step <<= 1;
+  return (bytes + step - 1) / step * step;
+}
+
 void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
-  bytes = (bytes + 511) & ~size_t(511);
+  bytes = size_class((bytes + 511) & ~size_t(511));
   // best fit among cached blocks, wasting at most half of a small block and
   // an eighth of a large one (config-4-sized products run within a few GB of
   // the device's capacity: 2x blocks of several GB each exhausted it)
@@ -67,10 +82,19 @@ void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
   }
   void* p = nullptr;
   cudaError_t e = cudaMalloc(&p, bytes);
-  if (e == cudaErrorMemoryAllocation) {
+  if (e == cudaErrorMemoryAllocation && !free_blocks.empty()) {
+    // out of memory: return cached blocks to the driver, largest first, only
+    // until the request fits
     cudaGetLastError();
-    trim(s);
-    e = cudaMalloc(&p, bytes);
+    cudaStreamSynchronize(s);
+    while (e == cudaErrorMemoryAllocation && !free_blocks.empty()) {
+      auto last = std::prev(free_blocks.end());
+      cudaFree(last->second);
+      reserved -= last->first;
+      free_blocks.erase(last);
+      e = cudaMalloc(&p, bytes);
+      if (e == cudaErrorMemoryAllocation) cudaGetLastError();
+    }
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
