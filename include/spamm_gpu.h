@@ -88,7 +88,7 @@ int spg_context_launch_count(spg_context* ctx, int64_t* launches);
 /* Products larger than the device's memory (the reference's spamm_multiply
  * has no size cap, multiply.cpp:109-116): when a product's task list (16 B
  * per candidate leaf product, 24 B for the L = 32 super-block entries; ~40 /
- * ~96 B where the expansion + sort builder runs: depth < 3 or > 12, chunks
+ * ~96 B where the expansion + sort builder runs: depth < 3, chunks
  * thinner than 8 block rows) would exceed `bytes` -- 0 (default):
  * half of the free HBM plus the context's cached pool -- the product is run
  * in 2^c row chunks, one task list at a time, into one C; bitwise the same C

@@ -8,7 +8,7 @@
 // below a child's (sqrt(fl(x*x)) < x for subnormal squares) skips exactly what
 // the reference skips.  K5 takes, per output block in Morton order, the
 // [begin, end) range of its (A slot, B slot) pairs with k ascending: for
-// trees of depth 3 .. 12 a dense walk per output tile produces them directly
+// trees of depth 3 .. 14 a dense walk per output tile produces them directly
 // in that order (below: tl_valid / tl_tile / tl_super); otherwise the tree is
 // expanded level by level, the leaf level writes sort keys
 // (Morton(i,j) << depth) | k, a deterministic radix sort groups them and run
@@ -155,7 +155,7 @@ __global__ void triples_to_keys(const int32_t* __restrict__ I, const int32_t* __
 //      expansion, sort, head flags and slot lookups per step -> see DESIGN).
 // The decisions are the same keep_pair tests on the same norms, so the set is
 // the expansion's bit for bit (tests: every survivor-set parity case, and the
-// old path stays behind SPG_TASKLIST=lists and for depth < 3 or > 12).
+// old path stays behind SPG_TASKLIST=lists and for depth < 3).
 constexpr int kTlWarps = 8;
 
 template <KeepRule R>
@@ -168,7 +168,7 @@ __global__ void tl_valid(int s, const double* __restrict__ pyrA, const double* _
   const uint32_t K = static_cast<uint32_t>(x) & ((1u << s) - 1u);
   const uint32_t J = static_cast<uint32_t>(x >> s) & ((1u << s) - 1u);
   const uint32_t I = row_lo + static_cast<uint32_t>(x >> (2 * s));
-  constexpr int kMaxS = 10;
+  constexpr int kMaxS = 12;  // levels 0 .. s, s <= 11
   double na[kMaxS], nb[kMaxS];
 #pragma unroll
   for (int l = 0; l < kMaxS; ++l) {
@@ -471,6 +471,15 @@ int tile_parts_log(const spg_context* ctx, int64_t n_tiles, int s) {
   return pl;
 }
 
+// The dense walk covers trees of depth 3 .. 14 (every depth the Morton grids
+// allow) while the flags of a shard's tiles, one byte per (tile, K), stay
+// below 8 GB: depth 14 unsharded is 8^11 of them.
+bool dense_walk_fits(int depth, int shard_level) {
+  const int s = depth - 3;
+  if (s < 0 || s > 11 || shard_level > s) return false;
+  return (3 * s - shard_level) <= 33;
+}
+
 // developer switch SPG_TASKLIST=lists: the top-down expansion + radix sort
 bool dense_tasklist_enabled() {
   static const bool on = [] {
@@ -487,8 +496,8 @@ struct DenseTasks {
   DevBuf<int2> pairs;
 };
 
-// The dense path applies to trees of depth 3 .. 12 and shards of whole tile
-// rows; false = use the expansion.  want_keys / want_pairs choose the outputs
+// The dense path applies to trees of depth 3 .. 14 (dense_walk_fits) and
+// shards of whole tile rows; false = use the expansion.  want_keys / want_pairs choose the outputs
 // (pairs with their per-block ranges out_keys / out_offset).
 template <KeepRule R>
 bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, double tau,
@@ -496,7 +505,7 @@ bool dense_tasklist(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, 
                     DenseTasks* out, bool want_blocks = false) {
   want_blocks = want_blocks || want_pairs;
   const int d = a->depth, s = d - 3;
-  if (!dense_tasklist_enabled() || s < 0 || s > 9 || sh.level > s) return false;
+  if (!dense_tasklist_enabled() || !dense_walk_fits(d, sh.level)) return false;
   PhaseTrace tr(ctx, "tasklist.dense");
   const uint32_t tile_rows = (1u << s) >> sh.level;
   const uint32_t row_lo = tile_rows * static_cast<uint32_t>(sh.index), row_hi = row_lo + tile_rows;
@@ -1416,7 +1425,7 @@ void stream_product_to_host(spg_context* ctx, const spg_matrix* a, const spg_mat
 // time.  Peak device bytes per candidate leaf product of a plan, against half
 // of the free memory (plus this context's cached blocks) left after `reserve`
 // bytes for the output, whose chunks accumulate:
-//  * dense walk (depth 3 .. 12, chunks of whole tile rows): 16 B -- a key and
+//  * dense walk (depth 3 .. 14, chunks of whole tile rows): 16 B -- a key and
 //    a slot pair per survivor; 24 B for the L = 32 super-block entries (slots,
 //    mask and k per entry, at most one entry per survivor);
 //  * expansion + radix sort (other depths, or chunks thinner than a tile row):
@@ -1449,7 +1458,7 @@ int chunk_bits(spg_context* ctx, const spg_matrix* a, const spg_matrix* b, Shard
   }();
   const int s = a->depth - 3;
   int c = -1;
-  if (dense_tasklist_enabled() && s >= 0 && s <= 9 && sh.level <= s)
+  if (dense_tasklist_enabled() && dense_walk_fits(a->depth, sh.level))
     c = bits_for(super32 ? 24.0 : 16.0, std::min(max_bits, s - sh.level));
   if (c < 0) {
     c = bits_for(super32 ? 96.0 : 40.0, max_bits);

@@ -292,6 +292,44 @@ def test_gemm_paths_in_subprocesses(env):
     assert run(env) == run({})
 
 
+@pytest.mark.parametrize("n,L", [(16384, 2), (32768, 2), (24000, 4)])
+def test_deep_trees_task_list_and_sweep(ctx, port, n, L):
+    """Quadtrees of depth 13 and 14 (the deepest the Morton grids allow), banded
+    with decaying blocks: the dense task-list walk (flags per (tile, K) up to
+    8^11) gives the oracle's survivor set, the product its C~, and the sweep
+    (pair lists at this depth) its bounds."""
+    from paper_2005_10680_b200 import _native as nat
+    from paper_2005_10680_b200.inputs import log_grid
+    rng = np.random.default_rng(n + L)
+    nb = -(-n // L)
+    off = np.arange(-3, 4)
+    r = np.repeat(np.arange(nb), len(off))
+    c = r + np.tile(off, nb)
+    keep = (c >= 0) & (c < nb) & (rng.random(len(r)) < 0.9)
+    r, c = r[keep].astype(np.int32), c[keep].astype(np.int32)
+    pay = rng.uniform(-1, 1, (len(r), L * L)) * (10.0 ** (-1.5 * np.abs(r - c)))[:, None]
+    if n % L:  # zero padding of the ragged last block row / column
+        blk = pay.reshape(len(r), L, L)  # column-major leaves: [col][row]
+        blk[r == nb - 1, :, n % L:] = 0.0
+        blk[c == nb - 1, n % L:, :] = 0.0
+    A = nat.upload(ctx, n, L, r, c, pay)
+    ta = port.build(n, L, r, c, pay)
+    tau = 1e-3
+    got = nat.survivors(ctx, A, A, tau)
+    want = port.survivors(ta, ta, tau)
+    assert len(got) == len(want) and len(want) > 0
+    key = lambda t: np.lexsort((t[:, 2], t[:, 1], t[:, 0]))  # noqa: E731
+    assert np.array_equal(got[key(got)], want[key(want)])
+    C, st = nat.spamm(ctx, A, A, tau)
+    assert st["survivors"] == len(want) and st["survivors"] < st["candidates"]
+    rc, cc, pc, _ = C.download()
+    wr, wc, wp, _ = port.spamm(ta, ta, tau).leaves()
+    assert np.array_equal(rc, wr) and np.array_equal(cc, wc)
+    assert rel_fro(pc, wp) < REL_TOL
+    taus = log_grid(32, 1.0, 1e-10)
+    assert bits_equal(nat.cse(ctx, A, A, taus), port.cse(ta, ta, taus))
+
+
 def test_run_to_run_determinism(ctx):
     """SPEC determinism (test_multiply.cpp:140-156 analogue): repeated calls are
     bitwise identical."""
